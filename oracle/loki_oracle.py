@@ -344,3 +344,15 @@ def sets_match_outside_band(gpu_idx, ref_idx, band) -> bool:
     gm[g] = True
     rm[r] = True
     return bool(np.array_equal(gm[out_band], rm[out_band]))
+
+
+def attend_on(q_hat, K_hat, V, indices):
+    """Exact attention restricted to a given selection: gathered scores / sqrt(D),
+    fp64 softmax, gathered weighted sum (attention.py:182-184).  Used when a GPU
+    selection differs from the oracle's only inside the tie band."""
+    q = np.asarray(q_hat, dtype=F32).reshape(-1)
+    K = np.asarray(K_hat, dtype=F32)
+    idx = np.asarray(indices, dtype=np.int64).reshape(-1)
+    exact = gathered_scores(q, K, idx) / F32(math.sqrt(K.shape[1]))
+    w = softmax_row(exact.astype(F32))
+    return gathered_wsum(w, V, idx), w

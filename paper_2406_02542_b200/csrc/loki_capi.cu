@@ -1,0 +1,305 @@
+// C ABI entry points (include/loki_b200.h): host-side validation with the
+// reference's error classes and messages, launch planning, dispatch.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "loki_common.cuh"
+#include "loki_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+loki_status fail(loki_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+loki_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return LOKI_OK;
+  return fail(LOKI_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+  return n;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+constexpr int kThreads = 256;
+constexpr size_t kSmemPreferred = 100 * 1024;
+constexpr size_t kSmemMax = 200 * 1024;
+
+int k_for(const loki_decode_args* a, int S) {
+  if (a->select_mode == LOKI_SELECT_ALL) return S;
+  if (a->k_fixed > 0) return a->k_fixed < S ? a->k_fixed : S;
+  return loki::resolve_fraction(a->k_f, S);
+}
+
+loki_status validate(const loki_decode_args* a) {
+  if (a == nullptr) return fail(LOKI_ERR_SHAPE, "null argument block");
+  const loki_kv_geom& g = a->g;
+  if (g.B < 1 || g.Hq < 1 || g.Hkv < 1 || g.D < 1 || g.S_cap < 1)
+    return fail(LOKI_ERR_SHAPE, "invalid geometry B=%d Hq=%d Hkv=%d D=%d S_cap=%d", g.B, g.Hq, g.Hkv, g.D, g.S_cap);
+  if (g.Hq % g.Hkv != 0)
+    return fail(LOKI_ERR_SHAPE, "query heads %d are not a multiple of kv heads %d", g.Hq, g.Hkv);
+  if (g.Hq / g.Hkv > 8) return fail(LOKI_ERR_UNSUPPORTED, "group size %d > 8", g.Hq / g.Hkv);
+  if (g.D > 256) return fail(LOKI_ERR_UNSUPPORTED, "head dim %d > 256", g.D);
+  if (g.dtype != LOKI_DTYPE_F32 && g.dtype != LOKI_DTYPE_BF16)
+    return fail(LOKI_ERR_UNSUPPORTED, "cache dtype code %d", g.dtype);
+  if (a->S_max < 1) return fail(LOKI_ERR_SHAPE, "attention needs at least one cached token");
+  if (a->S_max > g.S_cap) return fail(LOKI_ERR_SHAPE, "S_max %d exceeds cache capacity %d", a->S_max, g.S_cap);
+  if (a->lens == nullptr) return fail(LOKI_ERR_SHAPE, "lens is required");
+  if (a->select_mode < 0 || a->select_mode > 3) return fail(LOKI_ERR_DOMAIN, "select_mode %d", a->select_mode);
+  const bool computes_scores = a->ext_scores == nullptr &&
+                               (a->select_mode == LOKI_SELECT_TOPK || a->select_mode == LOKI_SELECT_NONE);
+  const bool attends = a->out != nullptr;
+  if (computes_scores || attends) {
+    if (a->q_hat == nullptr || a->K == nullptr) return fail(LOKI_ERR_SHAPE, "q_hat and K are required");
+    if (g.stride_s < g.D || g.stride_h < 0 || g.stride_b < 0)
+      return fail(LOKI_ERR_SHAPE, "cache strides (%lld, %lld, %lld) do not hold rows of %d",
+                  (long long)g.stride_b, (long long)g.stride_h, (long long)g.stride_s, g.D);
+  }
+  if (attends && a->V == nullptr) return fail(LOKI_ERR_SHAPE, "V is required");
+  if (computes_scores && (a->d < 1 || a->d > g.D)) return fail(LOKI_ERR_BUDGET, "d=%d outside [1, %d]", a->d, g.D);
+  if (a->select_mode != LOKI_SELECT_ALL && a->select_mode != LOKI_SELECT_NONE) {
+    if (a->k_fixed > a->S_max) return fail(LOKI_ERR_BUDGET, "k=%d outside [1, %d]", a->k_fixed, a->S_max);
+    if (a->k_fixed <= 0 && !(a->k_f > 0.0 && a->k_f <= 1.0))
+      return fail(LOKI_ERR_DOMAIN, "budget fraction must lie in (0, 1], got %g", a->k_f);
+  }
+  if (a->select_mode == LOKI_SELECT_NONE && a->approx_out == nullptr && !attends)
+    return fail(LOKI_ERR_SHAPE, "scores-only call without approx_out");
+  if (a->select_mode == LOKI_SELECT_NONE && attends)
+    return fail(LOKI_ERR_SHAPE, "scores-only call cannot attend");
+  if (a->select_mode == LOKI_SELECT_INDICES && a->ext_idx == nullptr)
+    return fail(LOKI_ERR_SHAPE, "external index lists are required");
+  if (a->select_mode == LOKI_SELECT_TOPK && !attends && a->idx_out == nullptr && a->approx_out == nullptr)
+    return fail(LOKI_ERR_SHAPE, "ranking-only call without outputs");
+  const bool needs_stride = a->ext_idx || a->idx_out || a->weights_out;
+  if (needs_stride) {
+    const int kmax = k_for(a, a->S_max);
+    if (a->idx_stride < kmax)
+      return fail(LOKI_ERR_SHAPE, "idx_stride %lld < k %d", (long long)a->idx_stride, kmax);
+  }
+  return LOKI_OK;
+}
+
+loki_status make_plan(const loki_decode_args* a, loki::Plan* plan, loki::FusedParams* p) {
+  const loki_kv_geom& g = a->g;
+  const int G = g.Hq / g.Hkv;
+  const int units = g.B * g.Hkv;
+  plan->G_T = loki::next_pow2(G);
+  plan->dtype = g.dtype;
+  const int vec = (g.dtype == LOKI_DTYPE_BF16) ? (plan->G_T == 8 ? 4 : 8) : 4;
+  const size_t vbytes = (size_t)vec * (g.dtype == LOKI_DTYPE_BF16 ? 2 : 4);
+  plan->fast = (g.D % vec == 0) && (g.D / vec <= 32) && (g.stride_s % vec == 0) && (g.stride_h % vec == 0) &&
+               (g.stride_b % vec == 0) && (a->K == nullptr || aligned(a->K, vbytes)) &&
+               (a->V == nullptr || aligned(a->V, vbytes));
+
+  const int target = 4 * sm_count();
+  auto smem_for = [&](int L, bool keys_smem) {
+    loki::FusedParams tmp{};
+    return loki::fused_layout(plan->G_T, kThreads, g.D, L, keys_smem, &tmp);
+  };
+  int C = 0;
+  bool keys_smem = true;
+  if (a->cluster_override > 0) {
+    C = a->cluster_override;
+    if (C != 1 && C != 2 && C != 4 && C != 8 && C != 16)
+      return fail(LOKI_ERR_DOMAIN, "cluster_override %d not in {1,2,4,8,16}", C);
+    const int L = loki::ceil_div(a->S_max, C);
+    keys_smem = smem_for(L, true) <= kSmemMax;
+  } else {
+    for (int c = 1; c <= 16; c *= 2) {
+      const int L = loki::ceil_div(a->S_max, c);
+      if (L > 65535) continue;
+      if (smem_for(L, true) > kSmemPreferred) continue;
+      if (units * c >= target || L <= 256 || c == 16) { C = c; break; }
+    }
+    if (C == 0) {
+      C = 16;
+      keys_smem = smem_for(loki::ceil_div(a->S_max, 16), true) <= kSmemMax;
+    }
+  }
+  const int L = loki::ceil_div(a->S_max, C);
+  if (L > 65535) return fail(LOKI_ERR_UNSUPPORTED, "sequence %d too long for %d CTAs per unit", a->S_max, C);
+  plan->C = C;
+  plan->Lmax = L < 1 ? 1 : L;
+  plan->keys_in_smem = keys_smem;
+  plan->smem = loki::fused_layout(plan->G_T, kThreads, g.D, plan->Lmax, keys_smem, p);
+  if (plan->smem > kSmemMax) return fail(LOKI_ERR_UNSUPPORTED, "shared memory plan %zu bytes", plan->smem);
+  plan->workspace = keys_smem ? 0 : (size_t)units * C * plan->G_T * plan->Lmax * 4;
+  return LOKI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* loki_last_error(void) { return g_last_error.c_str(); }
+
+int32_t loki_abi_version(void) { return LOKI_ABI_VERSION; }
+
+loki_status loki_device_check(int32_t device) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(LOKI_ERR_UNSUPPORTED, "device %d is sm_%d%d; libloki_b200 is built for sm_100a", device,
+                prop.major, prop.minor);
+  return LOKI_OK;
+}
+
+loki_status loki_decode_workspace_bytes(const loki_decode_args* a, size_t* bytes) {
+  loki_status s = validate(a);
+  if (s != LOKI_OK) return s;
+  loki::Plan plan;
+  loki::FusedParams p{};
+  s = make_plan(a, &plan, &p);
+  if (s != LOKI_OK) return s;
+  *bytes = plan.workspace;
+  return LOKI_OK;
+}
+
+loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, int32_t* rows_per_cta,
+                             size_t* smem_bytes) {
+  loki_status s = validate(a);
+  if (s != LOKI_OK) return s;
+  loki::Plan plan;
+  loki::FusedParams p{};
+  s = make_plan(a, &plan, &p);
+  if (s != LOKI_OK) return s;
+  if (ctas_per_unit) *ctas_per_unit = plan.C;
+  if (rows_per_cta) *rows_per_cta = plan.Lmax;
+  if (smem_bytes) *smem_bytes = plan.smem;
+  return LOKI_OK;
+}
+
+loki_status loki_decode(const loki_decode_args* a, void* stream) {
+  loki_status s = validate(a);
+  if (s != LOKI_OK) return s;
+  loki::Plan plan;
+  loki::FusedParams p{};
+  s = make_plan(a, &plan, &p);
+  if (s != LOKI_OK) return s;
+  if (plan.workspace > 0 && (a->workspace == nullptr || a->workspace_bytes < plan.workspace))
+    return fail(LOKI_ERR_SHAPE, "workspace of %zu bytes required", plan.workspace);
+  const loki_kv_geom& g = a->g;
+  p.q_hat = a->q_hat;
+  p.K = a->K;
+  p.V = a->V;
+  p.sb = g.stride_b;
+  p.sh = g.stride_h;
+  p.ss = g.stride_s;
+  p.B = g.B;
+  p.Hq = g.Hq;
+  p.Hkv = g.Hkv;
+  p.G = g.Hq / g.Hkv;
+  p.D = g.D;
+  p.S_cap = g.S_cap;
+  p.lens = a->lens;
+  p.d = a->d < 1 ? 1 : a->d;
+  p.k_f = a->k_f;
+  p.k_fixed = a->k_fixed;
+  p.select_mode = a->select_mode;
+  p.ext_scores = a->ext_scores;
+  p.ext_idx = a->ext_idx;
+  p.idx_stride = a->idx_stride;
+  p.out = a->out;
+  p.idx_out = a->idx_out;
+  p.approx_out = a->approx_out;
+  p.weights_out = a->weights_out;
+  p.C = plan.C;
+  p.Lmax = plan.Lmax;
+  p.keys_ws = plan.keys_in_smem ? nullptr : static_cast<uint32_t*>(a->workspace);
+  p.qscale = (float)(1.4426950408889634 / sqrt((double)g.D));
+  cudaError_t e = loki::launch_fused(p, plan, static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return cuda_status(e, "loki_decode launch");
+}
+
+loki_status loki_append_kv(const float* q_raw, const float* k_raw, const float* v_new, const float* P,
+                           int64_t P_head_stride, const double* inv_freq, const int64_t* positions,
+                           int32_t rope_mode, void* K, void* V, loki_kv_geom g, const int32_t* rows,
+                           float* q_hat_out, void* stream) {
+  if (g.B < 1 || g.Hq < 1 || g.Hkv < 1 || g.D < 1 || g.S_cap < 1 || g.Hq % g.Hkv != 0)
+    return fail(LOKI_ERR_SHAPE, "invalid geometry B=%d Hq=%d Hkv=%d D=%d", g.B, g.Hq, g.Hkv, g.D);
+  if (g.Hq / g.Hkv > 8) return fail(LOKI_ERR_UNSUPPORTED, "group size %d > 8", g.Hq / g.Hkv);
+  if (g.D > 256) return fail(LOKI_ERR_UNSUPPORTED, "head dim %d > 256", g.D);
+  if (g.dtype != LOKI_DTYPE_F32 && g.dtype != LOKI_DTYPE_BF16)
+    return fail(LOKI_ERR_UNSUPPORTED, "cache dtype code %d", g.dtype);
+  if (rope_mode < LOKI_ROPE_NONE || rope_mode > LOKI_ROPE_PROJECT_THEN_ROTATE)
+    return fail(LOKI_ERR_DOMAIN, "rope_mode %d", rope_mode);
+  if (rope_mode != LOKI_ROPE_NONE && (inv_freq == nullptr || g.D % 2 != 0))
+    return fail(LOKI_ERR_SHAPE, "head_dim must be a positive even number, got %d", g.D);
+  if (k_raw == nullptr || K == nullptr) return fail(LOKI_ERR_SHAPE, "k_raw and K are required");
+  if (v_new != nullptr && V == nullptr) return fail(LOKI_ERR_SHAPE, "V is required with v_new");
+  if (q_raw != nullptr && q_hat_out == nullptr) return fail(LOKI_ERR_SHAPE, "q_hat_out is required with q_raw");
+  cudaError_t e = loki::launch_append(q_raw, k_raw, v_new, P, P_head_stride, inv_freq, positions, rope_mode, K, V,
+                                      g, rows, q_hat_out, static_cast<cudaStream_t>(stream));
+  return cuda_status(e, "loki_append_kv launch");
+}
+
+loki_status loki_gathered_scores(const float* Q, int32_t M, const void* K, int64_t k_row_stride, int32_t dtype,
+                                 int32_t D, const int64_t* idx, int32_t n, float* out, void* stream) {
+  if (M < 1 || D < 1 || n < 0 || k_row_stride < D) return fail(LOKI_ERR_SHAPE, "invalid gathered-score shape");
+  if (dtype != LOKI_DTYPE_F32 && dtype != LOKI_DTYPE_BF16) return fail(LOKI_ERR_UNSUPPORTED, "dtype %d", dtype);
+  cudaError_t e = loki::launch_gathered_scores(Q, M, K, k_row_stride, dtype, D, idx, n, out,
+                                               static_cast<cudaStream_t>(stream));
+  return cuda_status(e, "loki_gathered_scores launch");
+}
+
+size_t loki_weighted_sum_workspace(int32_t n, int32_t D) {
+  const int nsplit = loki::ceil_div(n > 0 ? n : 1, 256);
+  return (size_t)nsplit * (D > 0 ? D : 1) * sizeof(float);
+}
+
+loki_status loki_weighted_sum(const float* w, const void* V, int64_t v_row_stride, int32_t dtype, int32_t D,
+                              const int64_t* idx, int32_t n, float* out, void* partial, size_t partial_bytes,
+                              void* stream) {
+  if (D < 1 || n < 0 || v_row_stride < D) return fail(LOKI_ERR_SHAPE, "invalid weighted-sum shape");
+  if (dtype != LOKI_DTYPE_F32 && dtype != LOKI_DTYPE_BF16) return fail(LOKI_ERR_UNSUPPORTED, "dtype %d", dtype);
+  if (partial == nullptr || partial_bytes < loki_weighted_sum_workspace(n, D))
+    return fail(LOKI_ERR_SHAPE, "partial workspace of %zu bytes required", loki_weighted_sum_workspace(n, D));
+  const int nsplit = loki::ceil_div(n > 0 ? n : 1, 256);
+  cudaError_t e = loki::launch_weighted_sum(w, V, v_row_stride, dtype, D, idx, n, out, static_cast<float*>(partial),
+                                            nsplit, static_cast<cudaStream_t>(stream));
+  return cuda_status(e, "loki_weighted_sum launch");
+}
+
+loki_status loki_softmax_rows(const float* x, int64_t rows, int32_t n, int64_t stride, float* out, void* stream) {
+  if (n < 1) return fail(LOKI_ERR_SHAPE, "softmax_row expects a nonempty vector");
+  if (rows < 0 || stride < n) return fail(LOKI_ERR_SHAPE, "invalid softmax shape");
+  cudaError_t e = loki::launch_softmax_rows(x, rows, n, stride, out, static_cast<cudaStream_t>(stream));
+  return cuda_status(e, "loki_softmax_rows launch");
+}
+
+loki_status loki_rope(const void* x, void* out, int32_t io_dtype, int64_t n_rows, int32_t D,
+                      const int64_t* positions, const double* inv_freq, void* stream) {
+  if (D <= 0 || D % 2 != 0) return fail(LOKI_ERR_SHAPE, "head_dim must be a positive even number, got %d", D);
+  if (io_dtype != LOKI_DTYPE_F32 && io_dtype != LOKI_DTYPE_F64)
+    return fail(LOKI_ERR_UNSUPPORTED, "rope dtype %d", io_dtype);
+  if (n_rows < 0 || positions == nullptr || inv_freq == nullptr) return fail(LOKI_ERR_SHAPE, "invalid rope arguments");
+  cudaError_t e = loki::launch_rope(x, out, io_dtype, n_rows, D, positions, inv_freq,
+                                    static_cast<cudaStream_t>(stream));
+  return cuda_status(e, "loki_rope launch");
+}
+
+loki_status loki_index_status(const int64_t* idx, int32_t n, int64_t bound, int32_t* status, void* stream) {
+  if (n < 0 || status == nullptr) return fail(LOKI_ERR_SHAPE, "invalid index-status arguments");
+  cudaError_t e = loki::launch_index_status(idx, n, bound, status, static_cast<cudaStream_t>(stream));
+  return cuda_status(e, "loki_index_status launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,450 @@
+"""GPU parity: libloki_b200 (sm_100a) against the pinned CPU oracle and the
+reference's golden vectors.  Every call goes through the C ABI.
+
+Bars (BASELINE north star / SURVEY 8c O4):
+  - top-k on given scores: bit-exact index sets (ties lowest-index-first);
+  - approx-score selections: identical outside the fp32 tie band;
+  - outputs: rel_err <= 1e-3 fp32 / bf16-vs-rounded-inputs, 2e-2 bf16-vs-fp32
+    (rel_err = max|a - e| / max|e|, tests/oracles.py:91-95);
+  - degeneration d = D, k = S vs vanilla within 1e-5.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from golden_inputs import gaussian_case, loki_case
+from oracle import loki_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+L = pytest.importorskip("paper_2406_02542_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+DEV = "cuda"
+
+
+def check_sets_and_outputs(q_hat, K_hat, V, lens, d, k_list, idx_gpu, y_gpu, tol, bf16=False):
+    """Per (b, h): selection vs oracle outside the tie band; output vs oracle
+    (re-evaluated on the GPU's own set when a band swap happened)."""
+    B, Hq, D = q_hat.shape
+    G = Hq // K_hat.shape[1]
+    swaps = 0
+    for b in range(B):
+        S = int(lens[b])
+        k = int(k_list[b])
+        for h in range(Hq):
+            Kb, Vb = K_hat[b, h // G, :S], V[b, h // G, :S]
+            y_ref, ref_idx, _, _ = O.loki_rank_and_attend(q_hat[b, h], Kb, Vb, d, k)
+            got = idx_gpu[b, h, :k]
+            band = O.tie_band(q_hat[b, h], Kb, d, k)
+            assert O.sets_match_outside_band(got, ref_idx, band), (b, h, S, k)
+            assert np.all(np.diff(got) > 0), "indices must be strictly ascending"
+            if not np.array_equal(got, ref_idx):
+                swaps += 1
+                y_ref = O.attend_on(q_hat[b, h], Kb, Vb, got)[0]
+            err = O.rel_err(y_gpu[b, h], y_ref)
+            assert err <= tol, (b, h, err)
+    return swaps
+
+
+# ------------------------------------------------------------------ golden
+
+
+def test_hand4_golden_tsv(golden):
+    P = golden["hand4/P"]
+    K_hat = np.ascontiguousarray(golden["hand4/keys"] @ P, dtype=np.float32)
+    for qi, q in enumerate(golden["hand4/queries"]):
+        y, diag = L.loki_rank_and_attend(np.asarray(q @ P, np.float32), K_hat, golden["hand4/values"], 2, 2)
+        assert diag.indices.tolist() == golden["hand4/tsv_idx"][qi].tolist()
+        assert np.abs(y - golden["hand4/tsv_y"][qi]).max() <= 1e-5
+
+
+def test_topk_bit_exact_vs_reference(golden):
+    offs, roffs = golden["topk/offsets"], golden["topk/ref_offsets"]
+    flat, ref = golden["topk/scores"], golden["topk/ref_flat"]
+    for i, k in enumerate(golden["topk/k"]):
+        s = torch.from_numpy(flat[offs[i]:offs[i + 1]]).to(DEV)
+        got = L.topk_indices(s, int(k)).cpu().numpy()
+        assert got.tolist() == ref[roffs[i]:roffs[i + 1]].tolist(), (i, int(k), s.numel())
+
+
+def test_topk_large_rows_and_ties():
+    rng = np.random.default_rng(5)
+    for n in (65536, 131072, 300000):
+        for quant in (None, 0):
+            s = rng.standard_normal(n)
+            if quant is not None:
+                s = np.round(s, quant)
+            s = s.astype(np.float32)
+            for k in (1, n // 4, n - 3):
+                got = L.topk_indices(torch.from_numpy(s).to(DEV), k).cpu().numpy()
+                assert np.array_equal(got, O.topk_indices(s, k)), (n, quant, k)
+
+
+def test_softmax_vs_reference(golden):
+    offs = golden["softmax/offsets"]
+    for i in range(offs.size - 1):
+        z = golden["softmax/flat"][offs[i]:offs[i + 1]]
+        got = L.softmax_row(z)
+        assert np.abs(got - golden["softmax/ref_flat"][offs[i]:offs[i + 1]]).max() <= 1e-7
+
+
+@pytest.mark.parametrize("S", [1, 2, 1000, 2048, 3000, 4095])
+def test_function_level_kernels_vs_reference(golden, S):
+    rng, q, K, V = gaussian_case(S, 128, S)
+    for d in (1, 17, 32, 128):
+        assert O.rel_err(L.sliced_score_kernel(q, K, d), golden[f"kern/S{S}/sliced_d{d}"]) <= 1e-4
+    idx = golden[f"kern/S{S}/idx"]
+    assert O.rel_err(L.gathered_score_kernel(q, K, idx), golden[f"kern/S{S}/gathered"]) <= 1e-4
+    assert O.rel_err(L.gathered_weighted_sum_kernel(golden[f"kern/S{S}/w"], V, idx),
+                     golden[f"kern/S{S}/wsum"]) <= 1e-4
+    assert O.rel_err(L.dense_weighted_sum_kernel(golden[f"kern/S{S}/wd"], V), golden[f"kern/S{S}/dense_wsum"]) <= 1e-4
+
+
+def test_query_block_kernels(golden):
+    Q, K, idx = golden["kern/block/Q"], golden["kern/block/K"], golden["kern/block/idx"]
+    blk = L.sliced_score_kernel(Q, K, 9)
+    assert O.rel_err(blk, golden["kern/block/sliced_d9"]) <= 1e-4
+    g = L.gathered_score_kernel(Q, K, idx)
+    assert O.rel_err(g, golden["kern/block/gathered"]) <= 1e-4
+    for i in range(Q.shape[0]):  # block rows equal per-row calls (test_kernels.py:125-134)
+        assert np.array_equal(blk[i], L.sliced_score_kernel(Q[i], K, 9))
+        assert np.array_equal(g[i], L.gathered_score_kernel(Q[i], K, idx))
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_loki_rank_and_attend_golden(golden, i):
+    c = loki_case(golden, i)
+    y, diag = L.loki_rank_and_attend(c["q_hat"], c["K_hat"], c["V"], c["d"], c["k"])
+    ref_idx = golden[f"loki/{i}/idx"]
+    band = O.tie_band(c["q_hat"], c["K_hat"], c["d"], c["k"])
+    assert O.sets_match_outside_band(diag.indices, ref_idx, band)
+    assert O.rel_err(diag.approx_scores, golden[f"loki/{i}/approx"]) <= 1e-5
+    y_ref = golden[f"loki/{i}/y"]
+    w_ref = golden[f"loki/{i}/weights"]
+    if not np.array_equal(diag.indices, ref_idx):
+        y_ref, w_ref = O.attend_on(c["q_hat"], c["K_hat"], c["V"], diag.indices)
+    assert O.rel_err(y, y_ref) <= 1e-4
+    assert np.abs(diag.weights - w_ref).max() <= 1e-5
+    yv, wv = L.vanilla_attention(c["q"], c["K"], c["V"])
+    assert O.rel_err(yv, golden[f"loki/{i}/vanilla_y"]) <= 1e-4
+    assert abs(float(wv.sum()) - 1.0) <= 1e-5
+    ye, ie = L.exact_topk_attention(c["q"], c["K"], c["V"], c["k"])
+    band = O.tie_band(c["q"], c["K"], c["D"], c["k"])
+    assert O.sets_match_outside_band(ie, golden[f"loki/{i}/exact_idx"], band)
+    if np.array_equal(ie, golden[f"loki/{i}/exact_idx"]):
+        assert O.rel_err(ye, golden[f"loki/{i}/exact_y"]) <= 1e-4
+
+
+@pytest.mark.parametrize("base", [10000, 500000])
+@pytest.mark.parametrize("D", [16, 128])
+def test_rope_vs_reference(golden, base, D):
+    tag = f"rope/b{base}/D{D}"
+    params = L.RopeParams(head_dim=D, base=float(base))
+    X, pos = golden[tag + "/x"], golden[tag + "/pos"]
+    out = np.stack([L.rope_apply(X[i], int(p), params) for i, p in enumerate(pos)])
+    assert O.rel_err(out, golden[tag + "/out"]) <= 1e-6
+    rows = L.rope_apply_rows(golden[tag + "/rows_x"], params, start_position=131060)
+    assert O.rel_err(rows, golden[tag + "/rows_out"]) <= 1e-6
+
+
+@pytest.mark.parametrize("base", [10000, 500000])
+@pytest.mark.parametrize("mode", ["ROTATE_THEN_PROJECT", "PROJECT_THEN_ROTATE"])
+def test_transform_step_vs_reference(golden, base, mode):
+    tag = f"xform/b{base}/{mode}"
+    D = 128
+    proj = L.ProjectionSet(0, 0, golden["xform/P"], np.ones(D, np.float32) / D, "pre")
+    params = L.RopeParams(head_dim=D, base=float(base))
+    for i, p in enumerate(golden[tag + "/pos"]):
+        qh, kh = L.transform_step(golden[tag + "/q"][i], golden[tag + "/k"][i], int(p), proj, params,
+                                  L.RotaryComposition[mode])
+        assert O.rel_err(qh, golden[tag + "/q_hat"][i]) <= 1e-5
+        assert O.rel_err(kh, golden[tag + "/k_hat"][i]) <= 1e-5
+
+
+def test_build_projection_vs_reference(golden):
+    for tag in ("calib/S256_D16", "calib/S8192_D128"):
+        S, D, r, sg, seed = golden[tag + "/spec"]
+        keys = O.gen_synthetic_keys(int(S), int(D), int(r), float(sg), int(seed))
+        proj = L.build_projection(keys, "post")
+        ev = golden[tag + "/eig"]
+        assert np.abs(proj.eigenvalues - ev).max() <= 1e-6
+        # eigenvectors of well-separated eigenvalues agree after canonical signs
+        sep = np.where(np.abs(np.diff(ev)) > 1e-3 * ev[0])[0]
+        for j in sep[:8]:
+            assert np.abs(proj.P[:, j] - golden[tag + "/P"][:, j]).max() <= 1e-4
+
+
+# ------------------------------------------------------------------ batched decode
+
+
+def make_batch(B, Hq, Hkv, D, S_cap, seed, rank=16, bf16=False):
+    rng = np.random.default_rng(seed)
+    keys = O.gen_synthetic_keys(S_cap + 512, D, rank, 1e-3, seed)
+    P, _ = O.build_projection(keys[:512])
+    base = keys[512:] @ P
+    K = np.empty((B, Hkv, S_cap, D), np.float32)
+    for b in range(B):
+        for g in range(Hkv):
+            K[b, g] = base[rng.permutation(S_cap)] * np.float32(1.0 + 0.05 * (b + g))
+    V = rng.standard_normal((B, Hkv, S_cap, D)).astype(np.float32)
+    q = rng.standard_normal((B, Hq, D)).astype(np.float32)
+    if bf16:
+        K, V = O.round_bf16(K), O.round_bf16(V)
+    return q, K, V
+
+
+CASES = [  # B, Hq, Hkv, D, S, k_f, d_f, dtype
+    (2, 4, 4, 128, 4096, 0.25, 0.25, "f32"),
+    (2, 4, 4, 128, 4096, 0.25, 0.25, "bf16"),
+    (2, 8, 2, 128, 3000, 0.125, 0.5, "bf16"),
+    (1, 8, 1, 128, 8192, 0.25, 0.25, "bf16"),
+    (3, 4, 2, 64, 1537, 0.3, 0.5, "f32"),
+    (1, 2, 1, 96, 999, 0.25, 0.25, "f32"),
+    (2, 2, 2, 128, 33, 0.5, 0.25, "bf16"),
+    (4, 4, 1, 128, 2048, 0.25, 0.25, "bf16"),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_batched_decode_vs_oracle(case):
+    B, Hq, Hkv, D, S, k_f, d_f, dt = case
+    bf = dt == "bf16"
+    q, K, V = make_batch(B, Hq, Hkv, D, S, seed=B * 1000 + S, bf16=bf)
+    tdt = torch.bfloat16 if bf else torch.float32
+    Kt = torch.from_numpy(K).to(DEV, tdt)
+    Vt = torch.from_numpy(V).to(DEV, tdt)
+    cfg = L.LokiConfig(k_f=k_f, d_f=d_f)
+    y, diag = L.loki_decode(torch.from_numpy(q).to(DEV), Kt, Vt, None, cfg=cfg, diagnostics=True)
+    d, k = cfg.resolve(D, S)
+    check_sets_and_outputs(q, K, V, [S] * B, d, [k] * B, diag.indices.cpu().numpy(), y.cpu().numpy(), 1e-3)
+    # approx diagnostics equal the sliced kernel within fp32 reassociation
+    for b in range(B):
+        for h in range(Hq):
+            a_ref = O.sliced_scores(q[b, h], K[b, h // (Hq // Hkv)], d)
+            assert O.rel_err(diag.approx_scores[b, h].cpu().numpy(), a_ref) <= 1e-5
+
+
+def test_bf16_vs_fp32_pipeline_tolerance():
+    q, K, V = make_batch(2, 4, 4, 128, 4096, seed=77)
+    cfg = L.LokiConfig(k_f=0.25, d_f=0.25)
+    y32 = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV), torch.from_numpy(V).to(DEV),
+                        None, cfg=cfg)
+    y16 = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+                        torch.from_numpy(V).to(DEV, torch.bfloat16), None, cfg=cfg)
+    assert O.rel_err(y16.cpu().numpy(), y32.cpu().numpy()) <= 2e-2
+
+
+def test_ragged_lengths():
+    B, Hq, Hkv, D, S_cap = 4, 4, 2, 128, 5000
+    q, K, V = make_batch(B, Hq, Hkv, D, S_cap, seed=11, bf16=True)
+    lens = [5000, 1, 4097, 77]
+    cfg = L.LokiConfig(k_f=0.25, d_f=0.25)
+    y, diag = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+                            torch.from_numpy(V).to(DEV, torch.bfloat16), lens, cfg=cfg, diagnostics=True)
+    d = cfg.resolve(D, 1)[0]
+    ks = [cfg.resolve(D, s)[1] for s in lens]
+    check_sets_and_outputs(q, K, V, lens, d, ks, diag.indices.cpu().numpy(), y.cpu().numpy(), 1e-3)
+
+
+@pytest.mark.parametrize("C", [1, 2, 4, 8, 16])
+def test_cluster_sizes_agree(C):
+    B, Hq, Hkv, D, S = 2, 4, 4, 128, 4099
+    q, K, V = make_batch(B, Hq, Hkv, D, S, seed=5, bf16=True)
+    args = (torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+            torch.from_numpy(V).to(DEV, torch.bfloat16), None)
+    y, diag = L.loki_decode(*args, d=32, k=1025, diagnostics=True, cluster=C)
+    y1, diag1 = L.loki_decode(*args, d=32, k=1025, diagnostics=True, cluster=1)
+    assert torch.equal(diag.indices, diag1.indices)
+    assert O.rel_err(y.cpu().numpy(), y1.cpu().numpy()) <= 1e-5
+    check_sets_and_outputs(q, K, V, [S] * B, 32, [1025] * B, diag.indices.cpu().numpy(), y.cpu().numpy(), 1e-3)
+
+
+def test_exact_ties_bit_exact():
+    """Integer-valued keys and queries make every fp32 sum exact, so the
+    selection must equal the reference rule bit for bit (massive ties)."""
+    rng = np.random.default_rng(3)
+    B, Hq, D, S = 2, 2, 64, 3001
+    K = rng.integers(-2, 3, size=(B, Hq, S, D)).astype(np.float32)
+    V = rng.standard_normal((B, Hq, S, D)).astype(np.float32)
+    q = rng.integers(-2, 3, size=(B, Hq, D)).astype(np.float32)
+    for d, k in ((4, 700), (8, 1), (16, 3000), (1, 1500)):
+        for C in (1, 4, 16):
+            y, diag = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV),
+                                    torch.from_numpy(V).to(DEV), None, d=d, k=k, diagnostics=True, cluster=C)
+            idx = diag.indices.cpu().numpy()
+            for b in range(B):
+                for h in range(Hq):
+                    ref = O.topk_indices(O.sliced_scores(q[b, h], K[b, h], d), k)
+                    assert np.array_equal(idx[b, h], ref), (d, k, C, b, h)
+
+
+def test_degeneration_full_budget_equals_vanilla():
+    rng = np.random.default_rng(202)
+    for S in (4, 17, 63, 1000):
+        q = rng.standard_normal(32).astype(np.float32)
+        K = rng.standard_normal((S, 32)).astype(np.float32)
+        V = rng.standard_normal((S, 32)).astype(np.float32)
+        y, diag = L.loki_rank_and_attend(q, K, V, 32, S)
+        y_ref, _ = O.vanilla_attention(q, K, V)
+        assert np.abs(y - y_ref).max() <= 1e-5
+        assert diag.indices.tolist() == list(range(S))
+        k = int(rng.integers(1, S + 1))
+        _, diag = L.loki_rank_and_attend(q, K, V, 32, k)
+        band = O.tie_band(q, K, 32, k)
+        assert O.sets_match_outside_band(diag.indices, O.topk_indices((K @ q).astype(np.float32), k), band)
+
+
+def test_dense_decode_matches_vanilla():
+    q, K, V = make_batch(2, 8, 2, 128, 2500, seed=9, bf16=True)
+    y = L.dense_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+                       torch.from_numpy(V).to(DEV, torch.bfloat16)).cpu().numpy()
+    for b in range(2):
+        for h in range(8):
+            y_ref, _ = O.vanilla_attention(q[b, h], K[b, h // 4], V[b, h // 4])
+            assert O.rel_err(y[b, h], y_ref) <= 1e-4
+
+
+def test_determinism():
+    q, K, V = make_batch(2, 4, 4, 128, 4096, seed=21, bf16=True)
+    args = (torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+            torch.from_numpy(V).to(DEV, torch.bfloat16), None)
+    a = L.loki_decode(*args, d=32, k=1024, diagnostics=True)
+    b = L.loki_decode(*args, d=32, k=1024, diagnostics=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1].indices, b[1].indices)
+    assert torch.equal(a[1].weights, b[1].weights)
+
+
+def test_long_sequence_global_key_store():
+    """S = 131072 with a GQA group of 8 exceeds on-chip key storage (C5 shape per unit)."""
+    B, Hq, Hkv, D, S = 1, 8, 1, 128, 131072
+    q, K, V = make_batch(B, Hq, Hkv, D, S, seed=131, bf16=True)
+    y, diag = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+                            torch.from_numpy(V).to(DEV, torch.bfloat16), None, d=32, k=32768, diagnostics=True)
+    check_sets_and_outputs(q, K, V, [S], 32, [32768], diag.indices.cpu().numpy(), y.cpu().numpy(), 1e-3)
+
+
+# ------------------------------------------------------------------ errors (same classes as the reference)
+
+
+def test_error_behaviour():
+    q = np.ones(8, np.float32)
+    K = np.ones((5, 8), np.float32)
+    with pytest.raises(L.BudgetError):
+        L.loki_rank_and_attend(q, K, K, 9, 2)
+    with pytest.raises(L.BudgetError):
+        L.loki_rank_and_attend(q, K, K, 4, 6)
+    with pytest.raises(L.ShapeError):
+        L.vanilla_attention(np.ones(4), np.ones((3, 5)), np.ones((3, 5)))
+    with pytest.raises(L.ShapeError):
+        L.loki_rank_and_attend(q, np.ones((0, 8), np.float32), np.ones((0, 8), np.float32), 1, 1)
+    with pytest.raises(IndexError):
+        L.gathered_score_kernel(q, K, [5])
+    with pytest.raises(L.ShapeError):
+        L.gathered_score_kernel(q, K, [3, 3])
+    with pytest.raises(L.BudgetError):
+        L.topk_indices([1.0, 2.0], 3)
+    with pytest.raises(L.ShapeError):
+        L.softmax_row(np.array([], np.float32))
+    with pytest.raises(L.ShapeError):
+        L.gathered_weighted_sum_kernel([0.5, 0.5], K, [1])
+
+
+# ------------------------------------------------------------------ cache / streaming
+
+
+def test_loki_attention_stream_matches_oracle_and_keeps_history():
+    D = 16
+    keys = O.gen_synthetic_keys(256, D, D, 0.0, 14)
+    P, eig = O.build_projection(keys)
+    proj = L.ProjectionSet(0, 0, P, eig, "post")
+    cache = L.KvCache(D, capacity=2)
+    rng = np.random.default_rng(15)
+    cfg = L.LokiConfig(k_f=0.5, d_f=0.5)
+    ks, vs = [], []
+    for t in range(50):
+        q, k, v = (rng.standard_normal(D).astype(np.float32) for _ in range(3))
+        y, diag = L.loki_attention(q, k, v, cache, proj, cfg)
+        ks.append((k @ P).astype(np.float32))
+        vs.append(v)
+        Kh = np.stack(ks)
+        dd, kk = cfg.resolve(D, t + 1)
+        y_ref, idx_ref, _, _ = O.loki_rank_and_attend((q @ P).astype(np.float32), Kh, np.stack(vs), dd, kk)
+        band = O.tie_band((q @ P).astype(np.float32), Kh, dd, kk)
+        assert O.sets_match_outside_band(diag.indices, idx_ref, band)
+        if np.array_equal(diag.indices, idx_ref):
+            assert O.rel_err(y, y_ref) <= 1e-4
+    assert len(cache) == 50
+    assert O.rel_err(cache.keys.cpu().numpy(), np.stack(ks)) <= 1e-6
+    assert np.array_equal(cache.values.cpu().numpy(), np.stack(vs))
+
+
+def test_cache_append_preserves_rows_bit_exact():
+    rng = np.random.default_rng(25)
+    cache = L.KvCache(8, capacity=1)
+    ks = rng.standard_normal((100, 8)).astype(np.float32)
+    vs = rng.standard_normal((100, 8)).astype(np.float32)
+    for i in range(100):
+        L.cache_append(cache, ks[i], vs[i])
+    assert np.array_equal(cache.keys.cpu().numpy(), ks)
+    assert np.array_equal(cache.values.cpu().numpy(), vs)
+    with pytest.raises(L.ShapeError):
+        cache.append(np.ones(3), np.ones(8))
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_decoder_step_with_rope_gqa(mode):
+    """LokiDecoder: K0 (RoPE + per-head P + append) then fused decode, vs oracle."""
+    B, Hq, Hkv, D, S0 = 2, 8, 2, 128, 2047
+    q0, K, V = make_batch(B, Hq, Hkv, D, S0 + 1, seed=40, bf16=True)
+    rng = np.random.default_rng(41)
+    Ps = []
+    for h in range(Hkv):
+        Ph, _ = O.build_projection(O.gen_synthetic_keys(600, D, 32, 1e-2, 50 + h))
+        Ps.append(Ph)
+    Pt = torch.from_numpy(np.stack(Ps)).to(DEV)
+    q_raw = rng.standard_normal((B, Hq, D)).astype(np.float32)
+    k_raw = rng.standard_normal((B, Hkv, D)).astype(np.float32)
+    v_new = rng.standard_normal((B, Hkv, D)).astype(np.float32)
+    Kt = torch.from_numpy(K).to(DEV, torch.bfloat16)
+    Vt = torch.from_numpy(V).to(DEV, torch.bfloat16)
+    rows = torch.full((B,), S0, dtype=torch.int32, device=DEV)
+    lens = torch.full((B,), S0 + 1, dtype=torch.int32, device=DEV)
+    pos = torch.tensor([S0, S0 + 100], dtype=torch.int64, device=DEV)
+    dec = L.LokiDecoder(Kt, Vt, Pt, Hq=Hq, d=32, k_f=0.25, rows=rows, lens=lens, S_max=S0 + 1,
+                        q_raw=torch.from_numpy(q_raw).to(DEV), k_raw=torch.from_numpy(k_raw).to(DEV),
+                        v_new=torch.from_numpy(v_new).to(DEV), rope_mode=mode, rope_base=500000.0, positions=pos)
+    y = dec.step().cpu().numpy()
+    torch.cuda.synchronize()
+    m = O.ROTATE_THEN_PROJECT if mode == 1 else O.PROJECT_THEN_ROTATE
+    q_hat = np.empty_like(q_raw)
+    Kc = Kt.float().cpu().numpy()
+    Vc = Vt.float().cpu().numpy()
+    G = Hq // Hkv
+    for b in range(B):
+        for g in range(Hkv):
+            _, kh = O.transform_step(q_raw[b, g * G], k_raw[b, g], int(pos[b]), Ps[g], 500000.0, m)
+            assert O.rel_err(Kc[b, g, S0], O.round_bf16(kh)) <= 1e-2
+            assert np.array_equal(Vc[b, g, S0], O.round_bf16(v_new[b, g]))
+        for h in range(Hq):
+            q_hat[b, h] = O.transform_step(q_raw[b, h], k_raw[b, h // G], int(pos[b]), Ps[h // G], 500000.0, m)[0]
+    assert O.rel_err(dec.q_hat.cpu().numpy(), q_hat) <= 1e-5
+    k = O.resolve_fraction(0.25, S0 + 1)
+    check_sets_and_outputs(dec.q_hat.cpu().numpy(), Kc, Vc, [S0 + 1] * B, 32, [k] * B,
+                           _topk_of(dec.q_hat, Kt, Vt, S0 + 1, k), y, 1e-3)
+
+
+def _topk_of(q_hat, Kt, Vt, S, k):
+    _, diag = L.loki_decode(q_hat, Kt, Vt, None, d=32, k=k, diagnostics=True)
+    return diag.indices.cpu().numpy()
