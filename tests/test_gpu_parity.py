@@ -237,13 +237,24 @@ def test_batched_decode_vs_oracle(case):
 
 
 def test_bf16_vs_fp32_pipeline_tolerance():
+    """bf16 cache vs the fp32 pipeline: on the selection the bf16 run made, the
+    output is within 2e-2 of fp32 arithmetic on the unrounded K / V; the
+    selections themselves agree to Jaccard >= 0.95 (rounding K_hat moves a few
+    boundary tokens, SURVEY 7 hard part 4)."""
     q, K, V = make_batch(2, 4, 4, 128, 4096, seed=77)
     cfg = L.LokiConfig(k_f=0.25, d_f=0.25)
-    y32 = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV), torch.from_numpy(V).to(DEV),
-                        None, cfg=cfg)
-    y16 = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
-                        torch.from_numpy(V).to(DEV, torch.bfloat16), None, cfg=cfg)
-    assert O.rel_err(y16.cpu().numpy(), y32.cpu().numpy()) <= 2e-2
+    qt = torch.from_numpy(q).to(DEV)
+    _, d32 = L.loki_decode(qt, torch.from_numpy(K).to(DEV), torch.from_numpy(V).to(DEV), None, cfg=cfg,
+                           diagnostics=True)
+    y16, d16 = L.loki_decode(qt, torch.from_numpy(K).to(DEV, torch.bfloat16),
+                             torch.from_numpy(V).to(DEV, torch.bfloat16), None, cfg=cfg, diagnostics=True)
+    y16 = y16.cpu().numpy()
+    i16, i32 = d16.indices.cpu().numpy(), d32.indices.cpu().numpy()
+    for b in range(2):
+        for h in range(4):
+            y_ref, _ = O.attend_on(q[b, h], K[b, h], V[b, h], i16[b, h])
+            assert O.rel_err(y16[b, h], y_ref) <= 2e-2
+            assert L.jaccard_topk(i16[b, h], i32[b, h]) >= 0.95
 
 
 def test_ragged_lengths():
