@@ -356,3 +356,44 @@ def attend_on(q_hat, K_hat, V, indices):
     exact = gathered_scores(q, K, idx) / F32(math.sqrt(K.shape[1]))
     w = softmax_row(exact.astype(F32))
     return gathered_wsum(w, V, idx), w
+
+
+# --------------------------------------------------------------------------
+# timing-faithful restatement for the CPU baseline (bench.py cpu_baseline leg)
+# --------------------------------------------------------------------------
+
+def topk_indices_partition(scores, k: int) -> np.ndarray:
+    """Same result as topk_indices, computed the reference's way: introselect
+    for the threshold, everything above it, ties lowest-index-first, sorted
+    (linalg.py:105-118).  O(S) like the reference, so the CPU timing is fair."""
+    s = np.asarray(scores).reshape(-1)
+    n = s.size
+    if k == n:
+        return np.arange(n, dtype=np.int64)
+    t = np.partition(s, n - k)[n - k]
+    above = np.flatnonzero(s > t)
+    ties = np.flatnonzero(s == t)[: k - above.size]
+    out = np.concatenate([above, ties])
+    out.sort()
+    return out.astype(np.int64, copy=False)
+
+
+def loki_unit_cpu(q_hat, K_hat, V, d: int, k: int):
+    """One (batch, head) unit of the reference's CPU path (attention.py:166-185)
+    with the O(S) selection; returns y only.  Used to time the CPU baseline."""
+    S, D = K_hat.shape
+    approx = K_hat[:, :d] @ q_hat[:d]
+    idx = topk_indices_partition(approx, k)
+    exact = (K_hat[idx] @ q_hat) / F32(math.sqrt(D))
+    z = exact.astype(F64)
+    e = np.exp(z - z.max())
+    w = (e / e.sum()).astype(F32)
+    return w @ V[idx]
+
+
+def dense_unit_cpu(q, K, V):
+    """One unit of vanilla_attention (attention.py:137-142); returns y only."""
+    logits = (K @ q) / F32(math.sqrt(K.shape[1]))
+    z = logits.astype(F64)
+    e = np.exp(z - z.max())
+    return (e / e.sum()).astype(F32) @ V

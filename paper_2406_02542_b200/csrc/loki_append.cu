@@ -132,15 +132,23 @@ cudaError_t launch_append(const float* q_raw, const float* k_raw, const float* v
   dim3 grid((unsigned)g.Hkv, (unsigned)ceil_div(g.B, kBatch));
   if (g.dtype == LOKI_DTYPE_BF16) {
     auto kern = append_kernel<__nv_bfloat16>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      smem_set = smem;
+    }
     kern<<<grid, kThreads, smem, st>>>(q_raw, k_raw, v_new, P, P_head_stride, inv_freq, positions, rope_mode,
                                        static_cast<__nv_bfloat16*>(K), static_cast<__nv_bfloat16*>(V), g,
                                        rows, q_hat_out);
   } else {
     auto kern = append_kernel<float>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      smem_set = smem;
+    }
     kern<<<grid, kThreads, smem, st>>>(q_raw, k_raw, v_new, P, P_head_stride, inv_freq, positions, rope_mode,
                                        static_cast<float*>(K), static_cast<float*>(V), g, rows, q_hat_out);
   }

@@ -648,11 +648,20 @@ size_t fused_layout(int G_T, int NT, int D, int Lmax, bool keys_in_smem, FusedPa
 template <typename T, int G_T, int VEC, int NCH, int NT>
 static cudaError_t launch_t(const FusedParams& p, int units, size_t smem, cudaStream_t st) {
   auto kern = fused_decode_kernel<T, G_T, VEC, NCH, NT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  if (p.C > 8) {
+  // attributes are process-wide per kernel: set them once (also keeps them out
+  // of CUDA-graph capture on the steady-state path)
+  static size_t smem_set = 0;
+  static bool nonportable_set = false;
+  cudaError_t e;
+  if (smem > smem_set) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  if (p.C > 8 && !nonportable_set) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
+    nonportable_set = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * p.C));

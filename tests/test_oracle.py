@@ -138,3 +138,19 @@ def test_tie_band_contains_threshold_and_is_small():
         assert 1 <= band.sum() <= 16
         idx = O.topk_indices(O.sliced_scores(q, K, d), k)
         assert O.sets_match_outside_band(idx, idx, band)
+
+
+def test_partition_topk_equals_sorted_topk(golden):
+    offs = golden["topk/offsets"]
+    flat = golden["topk/scores"]
+    for i, k in enumerate(golden["topk/k"]):
+        s = flat[offs[i]:offs[i + 1]]
+        assert np.array_equal(O.topk_indices_partition(s, int(k)), O.topk_indices(s, int(k)))
+
+
+def test_cpu_unit_matches_oracle(golden):
+    c = loki_case(golden, 4)
+    y = O.loki_unit_cpu(c["q_hat"], c["K_hat"], c["V"], c["d"], c["k"])
+    assert O.rel_err(y, golden["loki/4/y"]) <= 1e-5
+    yv = O.dense_unit_cpu(c["q"], c["K"], c["V"])
+    assert O.rel_err(yv, golden["loki/4/vanilla_y"]) <= 1e-5
