@@ -160,6 +160,12 @@ loki_status loki_rope(const void* x, void* out, int32_t io_dtype, int64_t n_rows
 loki_status loki_index_status(const int64_t* idx, int32_t n, int64_t bound, int32_t* status,
                               void* stream);
 
+/* Diagnostics: subsequent TMA-path loki_decode launches whose grid fits in
+ * max_ctas record eight %globaltimer stamps per CTA into buf [max_ctas][8]
+ * (start, phase 1 done, radix passes done, tie counts exchanged, selection
+ * emitted, union built, phase 3 done, end).  NULL disables. */
+loki_status loki_set_phase_trace(int64_t* buf, int32_t max_ctas);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,6 +1,7 @@
 // C ABI entry points (include/loki_b200.h): host-side validation with the
 // reference's error classes and messages, launch planning, dispatch.
 #include <math.h>
+#include <stdlib.h>
 #include <stdarg.h>
 #include <stdio.h>
 
@@ -8,6 +9,11 @@
 
 #include "loki_common.cuh"
 #include "loki_internal.h"
+
+namespace loki {
+long long* g_phase_trace = nullptr;
+int g_phase_trace_ctas = 0;
+}  // namespace loki
 
 namespace {
 
@@ -95,51 +101,133 @@ loki_status validate(const loki_decode_args* a) {
   return LOKI_OK;
 }
 
-loki_status make_plan(const loki_decode_args* a, loki::Plan* plan, loki::FusedParams* p) {
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (v == nullptr || *v == '\0') return dflt;
+  return atoi(v);
+}
+
+int stage_bytes_cfg() { return env_int("LOKI_TMA_STAGE_KB", 4) * 1024; }
+size_t smem_tma_target() { return (size_t)env_int("LOKI_SMEM_KB", 112) * 1024; }  // 112 KB: two CTAs per SM
+
+struct TmaGeom {
+  int vec, dbox, r1, r3;
+};
+
+// TMA plan pieces for (dtype, D, d, G_T); false when the layout is outside
+// what the TMA kernel handles.
+bool tma_geom(const loki_decode_args* a, int G_T, TmaGeom* t) {
+  const loki_kv_geom& g = a->g;
+  const int e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
+  const int vec = g.dtype == LOKI_DTYPE_BF16 ? (G_T == 8 ? 4 : 8) : 4;
+  if ((g.D * e) % 16 != 0 || g.D / vec > 32 || g.D % vec != 0) return false;
+  const int per16 = 16 / e;
+  const int d = a->d < 1 ? 1 : a->d;
+  const int dbox = loki::ceil_div(d, per16) * per16;
+  if (dbox > g.D && a->select_mode != LOKI_SELECT_ALL) return false;
+  // a stage is digested by one warp: phase 1 in passes of 4 x rpw1 rows,
+  // phase 3 in passes of 2 x rpw3 rows; gather4 needs multiples of 4 rows
+  const int rpw1 = 32 / loki::next_pow2(dbox / vec);
+  const int kStageBytes = stage_bytes_cfg();
+  int r1 = kStageBytes / (dbox * e);
+  if (r1 > 256) r1 = 256;
+  r1 = r1 / (4 * rpw1) * (4 * rpw1);
+  const int rpw3 = 32 / loki::next_pow2(g.D / vec);
+  int unit3 = 2 * rpw3;
+  while (unit3 % 4) unit3 *= 2;
+  int r3 = kStageBytes / (2 * g.D * e);
+  if (r3 > 32) r3 = 32;  // the producer warp resolves one gathered row per lane
+  r3 = r3 / unit3 * unit3;
+  if (r1 < 4 * rpw1 || r3 < unit3) return false;
+  t->vec = vec;
+  t->dbox = dbox;
+  t->r1 = r1;
+  t->r3 = r3;
+  return true;
+}
+
+loki_status make_plan(const loki_decode_args* a, loki::Plan* plan, loki::FusedParams* p, TmaGeom* tg) {
   const loki_kv_geom& g = a->g;
   const int G = g.Hq / g.Hkv;
   const int units = g.B * g.Hkv;
   plan->G_T = loki::next_pow2(G);
   plan->dtype = g.dtype;
   const int vec = (g.dtype == LOKI_DTYPE_BF16) ? (plan->G_T == 8 ? 4 : 8) : 4;
-  const size_t vbytes = (size_t)vec * (g.dtype == LOKI_DTYPE_BF16 ? 2 : 4);
+  const size_t ebytes = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
+  const size_t vbytes = (size_t)vec * ebytes;
   plan->fast = (g.D % vec == 0) && (g.D / vec <= 32) && (g.stride_s % vec == 0) && (g.stride_h % vec == 0) &&
                (g.stride_b % vec == 0) && (a->K == nullptr || aligned(a->K, vbytes)) &&
                (a->V == nullptr || aligned(a->V, vbytes));
 
-  const int target = 4 * sm_count();
+  // TMA path: cache reachable as one 2-D [B*Hkv*S_cap, D] row space, 16 B aligned
+  const bool contiguous = (g.Hkv == 1 || g.stride_h == (int64_t)g.S_cap * g.stride_s) &&
+                          (g.B == 1 || g.stride_b == (int64_t)g.Hkv * g.S_cap * g.stride_s);
+  plan->tma = env_int("LOKI_TMA", 1) != 0 && a->K != nullptr && a->V != nullptr && a->ext_scores == nullptr &&
+              contiguous && aligned(a->K, 16) && aligned(a->V, 16) && (g.stride_s * ebytes) % 16 == 0 &&
+              (long long)g.B * g.Hkv * g.S_cap < (1LL << 31) && loki::tma_supported(g.dtype, g.D, plan->G_T) &&
+              tma_geom(a, plan->G_T, tg);
+  const int kStageBytes = stage_bytes_cfg();
+  const int NTt = loki::kTmaThreads;
+  const int align = plan->tma ? tg->r1 : 1;
+  const int nst_env = env_int("LOKI_TMA_STAGES", 0);
+  auto Lfor = [&](int c) { return loki::ceil_div(loki::ceil_div(a->S_max, c), align) * align; };
+  // TMA: as many ring stages as fit next to the slice state in the per-CTA budget
+  auto stages_for = [&](int L, bool keys_smem) {
+    if (nst_env > 0) return nst_env;
+    loki::FusedParams tmp{};
+    const size_t base = loki::fused_tma_layout(plan->G_T, NTt, g.D, L, keys_smem, 0, kStageBytes, &tmp);
+    const long long per = (long long)kStageBytes * loki::kTmaWarps;  // one stage in every warp's ring
+    const long long n = base >= smem_tma_target() ? 0 : (long long)((smem_tma_target() - base) / per);
+    return (int)(n > 8 ? 8 : n);
+  };
   auto smem_for = [&](int L, bool keys_smem) {
     loki::FusedParams tmp{};
-    return loki::fused_layout(plan->G_T, kThreads, g.D, L, keys_smem, &tmp);
+    return plan->tma ? loki::fused_tma_layout(plan->G_T, NTt, g.D, L, keys_smem, stages_for(L, keys_smem) < 2 ? 2 : stages_for(L, keys_smem), kStageBytes, &tmp)
+                     : loki::fused_layout(plan->G_T, kThreads, g.D, L, keys_smem, &tmp);
   };
+  const size_t preferred = plan->tma ? smem_tma_target() : kSmemPreferred;
+  const int target = 4 * sm_count();
   int C = 0;
   bool keys_smem = true;
-  if (a->cluster_override > 0) {
-    C = a->cluster_override;
+  const int cov = a->cluster_override > 0 ? a->cluster_override : env_int("LOKI_CLUSTER", 0);
+  if (cov > 0) {
+    C = cov;
     if (C != 1 && C != 2 && C != 4 && C != 8 && C != 16)
       return fail(LOKI_ERR_DOMAIN, "cluster_override %d not in {1,2,4,8,16}", C);
-    const int L = loki::ceil_div(a->S_max, C);
-    keys_smem = smem_for(L, true) <= kSmemMax;
+    keys_smem = smem_for(Lfor(C), true) <= kSmemMax;
   } else {
     for (int c = 1; c <= 16; c *= 2) {
-      const int L = loki::ceil_div(a->S_max, c);
+      const int L = Lfor(c);
       if (L > 65535) continue;
-      if (smem_for(L, true) > kSmemPreferred) continue;
-      if (units * c >= target || L <= 256 || c == 16) { C = c; break; }
+      if (smem_for(L, true) > preferred) continue;
+      if (units * c >= target || L <= 256 || c == 16) {
+        C = c;
+        break;
+      }
     }
     if (C == 0) {
       C = 16;
-      keys_smem = smem_for(loki::ceil_div(a->S_max, 16), true) <= kSmemMax;
+      keys_smem = smem_for(Lfor(16), true) <= kSmemMax;
     }
   }
-  const int L = loki::ceil_div(a->S_max, C);
+  int nst = plan->tma ? stages_for(Lfor(C), keys_smem) : 0;
+  if (plan->tma && nst < 2) nst = 2;
+  const int L = Lfor(C);
   if (L > 65535) return fail(LOKI_ERR_UNSUPPORTED, "sequence %d too long for %d CTAs per unit", a->S_max, C);
   plan->C = C;
   plan->Lmax = L < 1 ? 1 : L;
   plan->keys_in_smem = keys_smem;
-  plan->smem = loki::fused_layout(plan->G_T, kThreads, g.D, plan->Lmax, keys_smem, p);
+  plan->smem = plan->tma ? loki::fused_tma_layout(plan->G_T, NTt, g.D, plan->Lmax, keys_smem, nst, kStageBytes, p)
+                         : loki::fused_layout(plan->G_T, kThreads, g.D, plan->Lmax, keys_smem, p);
   if (plan->smem > kSmemMax) return fail(LOKI_ERR_UNSUPPORTED, "shared memory plan %zu bytes", plan->smem);
   plan->workspace = keys_smem ? 0 : (size_t)units * C * plan->G_T * plan->Lmax * 4;
+  p->slice_align = align;
+  if (plan->tma) {
+    p->r1 = tg->r1;
+    p->dbox = tg->dbox;
+    p->r3 = tg->r3;
+    p->unit_rows = g.S_cap;
+  }
   return LOKI_OK;
 }
 
@@ -166,7 +254,8 @@ loki_status loki_decode_workspace_bytes(const loki_decode_args* a, size_t* bytes
   if (s != LOKI_OK) return s;
   loki::Plan plan;
   loki::FusedParams p{};
-  s = make_plan(a, &plan, &p);
+  TmaGeom tg{};
+  s = make_plan(a, &plan, &p, &tg);
   if (s != LOKI_OK) return s;
   *bytes = plan.workspace;
   return LOKI_OK;
@@ -178,7 +267,8 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
   if (s != LOKI_OK) return s;
   loki::Plan plan;
   loki::FusedParams p{};
-  s = make_plan(a, &plan, &p);
+  TmaGeom tg{};
+  s = make_plan(a, &plan, &p, &tg);
   if (s != LOKI_OK) return s;
   if (ctas_per_unit) *ctas_per_unit = plan.C;
   if (rows_per_cta) *rows_per_cta = plan.Lmax;
@@ -191,7 +281,8 @@ loki_status loki_decode(const loki_decode_args* a, void* stream) {
   if (s != LOKI_OK) return s;
   loki::Plan plan;
   loki::FusedParams p{};
-  s = make_plan(a, &plan, &p);
+  TmaGeom tg{};
+  s = make_plan(a, &plan, &p, &tg);
   if (s != LOKI_OK) return s;
   if (plan.workspace > 0 && (a->workspace == nullptr || a->workspace_bytes < plan.workspace))
     return fail(LOKI_ERR_SHAPE, "workspace of %zu bytes required", plan.workspace);
@@ -223,8 +314,19 @@ loki_status loki_decode(const loki_decode_args* a, void* stream) {
   p.C = plan.C;
   p.Lmax = plan.Lmax;
   p.keys_ws = plan.keys_in_smem ? nullptr : static_cast<uint32_t*>(a->workspace);
+  p.debug = env_int("LOKI_DEBUG", 0);
+  p.trace = (loki::g_phase_trace != nullptr && g.B * g.Hkv * plan.C <= loki::g_phase_trace_ctas)
+                ? loki::g_phase_trace : nullptr;
   p.qscale = (float)(1.4426950408889634 / sqrt((double)g.D));
-  cudaError_t e = loki::launch_fused(p, plan, static_cast<cudaStream_t>(stream));
+  cudaError_t e;
+  if (plan.tma) {
+    loki::TmaDesc maps[5];
+    if (!loki::encode_tma(a->K, a->V, g, tg.dbox, tg.r1, tg.r3, maps))
+      return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
+    e = loki::launch_fused_tma(p, plan, maps, static_cast<cudaStream_t>(stream));
+  } else {
+    e = loki::launch_fused(p, plan, static_cast<cudaStream_t>(stream));
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   return cuda_status(e, "loki_decode launch");
 }
@@ -294,6 +396,12 @@ loki_status loki_rope(const void* x, void* out, int32_t io_dtype, int64_t n_rows
   cudaError_t e = loki::launch_rope(x, out, io_dtype, n_rows, D, positions, inv_freq,
                                     static_cast<cudaStream_t>(stream));
   return cuda_status(e, "loki_rope launch");
+}
+
+loki_status loki_set_phase_trace(int64_t* buf, int32_t max_ctas) {
+  loki::g_phase_trace = reinterpret_cast<long long*>(buf);
+  loki::g_phase_trace_ctas = buf ? max_ctas : 0;
+  return LOKI_OK;
 }
 
 loki_status loki_index_status(const int64_t* idx, int32_t n, int64_t bound, int32_t* status, void* stream) {

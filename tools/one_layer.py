@@ -1,0 +1,83 @@
+"""One-layer timing / profiling driver (not part of the product).
+
+    python tools/one_layer.py [--B 16] [--H 32] [--Hkv 32] [--S 8192] [--mode loki|dense] [--reps 20]
+
+Builds a random bf16 cache, runs loki_decode (or dense) through the public
+batched API and prints per-launch CUDA-event time and achieved algorithmic GB/s.
+Env LOKI_TMA / LOKI_TMA_STAGES / LOKI_CLUSTER steer the launch plan.
+"""
+
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2406_02542_b200 as L  # noqa: E402
+from paper_2406_02542_b200 import _core, _lib  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--B", type=int, default=16)
+ap.add_argument("--H", type=int, default=32)
+ap.add_argument("--Hkv", type=int, default=32)
+ap.add_argument("--S", type=int, default=8192)
+ap.add_argument("--D", type=int, default=128)
+ap.add_argument("--kf", type=float, default=0.25)
+ap.add_argument("--df", type=float, default=0.25)
+ap.add_argument("--mode", default="loki")
+ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--cluster", type=int, default=0)
+a = ap.parse_args()
+
+dev = torch.device("cuda", 0)
+g = torch.Generator(device=dev)
+g.manual_seed(0)
+K = torch.randn(a.B, a.Hkv, a.S, a.D, device=dev, generator=g).to(torch.bfloat16)
+V = torch.randn(a.B, a.Hkv, a.S, a.D, device=dev, generator=g).to(torch.bfloat16)
+q = torch.randn(a.B, a.H, a.D, device=dev, generator=g)
+out = torch.empty(a.B, a.H, a.D, device=dev)
+lens = torch.full((a.B,), a.S, dtype=torch.int32, device=dev)
+d = max(1, min(a.D, int(a.df * a.D + 0.5)))
+k = max(1, min(a.S, int(a.kf * a.S + 0.5)))
+if a.mode == "dense":
+    call = _core.DecodeCall(q, K, V, lens, a.S, a.D, select_mode=_lib.SELECT_ALL, out=out, cluster=a.cluster)
+    nbytes = a.B * a.Hkv * a.S * a.D * 2 * 2
+else:
+    call = _core.DecodeCall(q, K, V, lens, a.S, d, k_fixed=k, out=out, cluster=a.cluster)
+    nbytes = a.B * a.Hkv * 2 * (d * a.S + 2 * a.D * k)
+print("plan", call.plan(), "TMA", os.environ.get("LOKI_TMA", "1"))
+for _ in range(3):
+    call.run()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.reps):
+    call.run()
+e1.record()
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1000 / a.reps
+print(f"{a.mode}: {us:.1f} us/launch, {nbytes / us / 1e3:.1f} GB/s algorithmic")
+
+if os.environ.get("LOKI_TRACE"):
+    import numpy as np
+
+    plan = call.plan()
+    ctas = a.B * a.Hkv * plan["ctas_per_unit"]
+    buf = torch.zeros(ctas * 8, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.loki_set_phase_trace(buf.data_ptr(), ctas))
+    call.run()
+    torch.cuda.synchronize()
+    _lib.check(lib.loki_set_phase_trace(None, 0))
+    t = buf.view(ctas, 8).cpu().numpy().astype(np.float64)
+    for i in range(1, 8):  # steps a path skipped keep the previous stamp
+        t[:, i] = np.where(t[:, i] == 0, t[:, i - 1], t[:, i])
+    t0 = t[:, 0].min()
+    t = (t - t0) / 1000.0  # us
+    dur = np.diff(t, axis=1)
+    names = ["phase1", "radix", "counts", "emit", "union", "phase3", "merge"]
+    print(f"kernel span {t[:, 7].max():.1f} us; CTA start spread {t[:, 0].max():.1f} us")
+    for i, n in enumerate(names):
+        print(f"  {n:7s} median {np.median(dur[:, i]):7.2f} us  mean {dur[:, i].mean():7.2f}  max {dur[:, i].max():7.2f}"
+              f"  sum-share {dur[:, i].sum() / dur.sum() * 100:5.1f}%")
