@@ -26,13 +26,16 @@ __device__ __forceinline__ void rope_pair(double lo, double hi, double theta, do
   ohi = __dadd_rn(__dmul_rn(lo, s), __dmul_rn(hi, c));
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 template <typename T, bool P_SMEM>
 __global__ void __launch_bounds__(kThreads) append_kernel(
     const float* __restrict__ q_raw, const float* __restrict__ k_raw, const float* __restrict__ v_new,
     const float* __restrict__ P, int64_t P_head_stride, const double* __restrict__ inv_freq,
     const int64_t* __restrict__ positions, int rope_mode, T* __restrict__ K, T* __restrict__ V,
     loki_kv_geom g, const int32_t* __restrict__ rows, float* __restrict__ q_hat_out) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t p_bar;
   const int hk = blockIdx.x;
   const int b0 = blockIdx.y * kBatch;
   const int D = g.D, half = D / 2;
@@ -40,23 +43,37 @@ __global__ void __launch_bounds__(kThreads) append_kernel(
   const int nb = min(kBatch, g.B - b0);
   const int per_b = (q_raw ? G : 0) + 1;  // vectors per batch: G queries then the key
   const int nv = nb * per_b;
+  const int nv4 = (nv + 3) & ~3;          // padded to whole float4 groups of vectors
   float* Ps = reinterpret_cast<float*>(smem_raw);           // [D][D] when P_SMEM
-  float* x = Ps + (P_SMEM && P ? (size_t)D * D : 0);       // [nv][D]
-  float* y = x + (size_t)nv * D;                            // [nv][D]
+  float* x = Ps + (P_SMEM && P ? (size_t)D * D : 0);       // [nv4][D], zero padded
+  float* y = x + (size_t)nv4 * D;                           // [nv4][D]
   const float* Ph = P ? P + (size_t)hk * P_head_stride : nullptr;
 
-  // PDL: everything above overlaps the previous kernel; inputs are read below
+  // P is a constant of the layer: its bulk copy starts before the PDL wait, so
+  // it overlaps the tail of the previous kernel
+  const bool stage_p = P_SMEM && Ph != nullptr;
+  if (stage_p && threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)(D * D * sizeof(float));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&p_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&p_bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(Ps)),
+        "l"(Ph), "r"(bytes), "r"(smem_addr(&p_bar))
+        : "memory");
+  }
+  // PDL: inputs (the previous layer's products in a real model) are read below
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (P_SMEM && Ph) {  // stage this head's P with 16-byte loads (L2-resident across batches)
-    const int n4 = D * D / 4;
-    const float4* src = reinterpret_cast<const float4*>(Ph);
-    float4* dst = reinterpret_cast<float4*>(Ps);
-    for (int i = threadIdx.x; i < n4; i += kThreads) dst[i] = __ldg(src + i);
-  }
   // gather inputs; rotate first when the composition is rotate-then-project
-  for (int i = threadIdx.x; i < nv * D; i += kThreads) {
+  for (int i = threadIdx.x; i < nv4 * D; i += kThreads) {
     const int v = i / D, col = i % D;
+    if (v >= nv) {
+      x[i] = 0.f;
+      continue;
+    }
     const int bl = v / per_b, slot = v % per_b;
     const int bb = b0 + bl;
     const float* src = (slot < per_b - 1)
@@ -75,30 +92,55 @@ __global__ void __launch_bounds__(kThreads) append_kernel(
       x[v * D + col] = src[col];
     }
   }
+  if (stage_p) {
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(ok)
+          : "r"(smem_addr(&p_bar))
+          : "memory");
+  }
   __syncthreads();
 
-  // y = x @ P (fp32 accumulate in index order, like the reference's float32 matmul)
+  // y = x @ P (fp32 accumulate in index order, like the reference's float32 matmul);
+  // four vectors per pass, four inputs per step: float4 broadcast reads of x
   for (int col = threadIdx.x; col < D; col += kThreads) {
-    for (int v0 = 0; v0 < nv; v0 += kVecChunk) {
-      float acc[kVecChunk];
-#pragma unroll
-      for (int u = 0; u < kVecChunk; ++u) acc[u] = 0.f;
-      if (Ph) {
-#pragma unroll 4
+    for (int v0 = 0; v0 < nv4; v0 += 4) {
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      if (Ph && (D & 3)) {  // odd widths: plain scalar walk
         for (int i = 0; i < D; ++i) {
           const float pij = P_SMEM ? Ps[i * D + col] : __ldg(Ph + (size_t)i * D + col);
+          a0 = fmaf(x[(v0 + 0) * D + i], pij, a0);
+          a1 = fmaf(x[(v0 + 1) * D + i], pij, a1);
+          a2 = fmaf(x[(v0 + 2) * D + i], pij, a2);
+          a3 = fmaf(x[(v0 + 3) * D + i], pij, a3);
+        }
+      } else if (Ph) {
+#pragma unroll 4
+        for (int i = 0; i < D; i += 4) {
+          float p4[4];
 #pragma unroll
-          for (int u = 0; u < kVecChunk; ++u)
-            if (v0 + u < nv) acc[u] = fmaf(x[(v0 + u) * D + i], pij, acc[u]);
+          for (int t = 0; t < 4; ++t) p4[t] = P_SMEM ? Ps[(i + t) * D + col] : __ldg(Ph + (size_t)(i + t) * D + col);
+          const float4 x0 = *reinterpret_cast<const float4*>(x + (v0 + 0) * D + i);
+          const float4 x1 = *reinterpret_cast<const float4*>(x + (v0 + 1) * D + i);
+          const float4 x2 = *reinterpret_cast<const float4*>(x + (v0 + 2) * D + i);
+          const float4 x3 = *reinterpret_cast<const float4*>(x + (v0 + 3) * D + i);
+          a0 = fmaf(x0.w, p4[3], fmaf(x0.z, p4[2], fmaf(x0.y, p4[1], fmaf(x0.x, p4[0], a0))));
+          a1 = fmaf(x1.w, p4[3], fmaf(x1.z, p4[2], fmaf(x1.y, p4[1], fmaf(x1.x, p4[0], a1))));
+          a2 = fmaf(x2.w, p4[3], fmaf(x2.z, p4[2], fmaf(x2.y, p4[1], fmaf(x2.x, p4[0], a2))));
+          a3 = fmaf(x3.w, p4[3], fmaf(x3.z, p4[2], fmaf(x3.y, p4[1], fmaf(x3.x, p4[0], a3))));
         }
       } else {
-#pragma unroll
-        for (int u = 0; u < kVecChunk; ++u)
-          if (v0 + u < nv) acc[u] = x[(v0 + u) * D + col];
+        a0 = x[(v0 + 0) * D + col];
+        a1 = x[(v0 + 1) * D + col];
+        a2 = x[(v0 + 2) * D + col];
+        a3 = x[(v0 + 3) * D + col];
       }
-#pragma unroll
-      for (int u = 0; u < kVecChunk; ++u)
-        if (v0 + u < nv) y[(v0 + u) * D + col] = acc[u];
+      y[(v0 + 0) * D + col] = a0;
+      y[(v0 + 1) * D + col] = a1;
+      y[(v0 + 2) * D + col] = a2;
+      y[(v0 + 3) * D + col] = a3;
     }
   }
   __syncthreads();
@@ -168,9 +210,9 @@ cudaError_t launch_append(const float* q_raw, const float* k_raw, const float* v
   const int G = g.Hq / g.Hkv;
   const int per_b = (q_raw ? G : 0) + 1;
   const bool p_smem = P != nullptr && g.D <= kSmemPMaxD && (reinterpret_cast<uintptr_t>(P) % 16) == 0 &&
-                      (P_head_stride % 4) == 0 && (g.D % 4) == 0;
-  const size_t smem = (size_t)2 * kBatch * per_b * g.D * sizeof(float) +
-                      (p_smem ? (size_t)g.D * g.D * sizeof(float) : 0);
+                      (P_head_stride % 4) == 0;
+  const size_t nv4 = ((size_t)kBatch * per_b + 3) & ~(size_t)3;
+  const size_t smem = (size_t)2 * nv4 * g.D * sizeof(float) + (p_smem ? (size_t)g.D * g.D * sizeof(float) : 0);
   dim3 grid((unsigned)g.Hkv, (unsigned)ceil_div(g.B, kBatch));
   cudaError_t e;
   if (g.dtype == LOKI_DTYPE_BF16)

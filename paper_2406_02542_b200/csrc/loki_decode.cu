@@ -207,7 +207,7 @@ size_t fused_layout(int G_T, int NT, int D, int Lmax, bool keys_in_smem, FusedPa
   const size_t keys = keys_in_smem ? (size_t)G_T * Lmax * 4 : 0;
   p->off_keys = (int)off; off = align_up(off + keys, 16);
   p->off_sel = (int)off; off = align_up(off + (size_t)Lmax, 16);
-  p->off_union = (int)off; off = align_up(off + (size_t)Lmax * 2, 16);
+  p->off_union = (int)off; off = align_up(off + align_up((size_t)Lmax, 1024) * 2, 16);
   p->off_hist = (int)off; off = align_up(off + (size_t)3 * G_T * kRadixBins * 4, 16);
   p->off_merge = (int)off; off = align_up(off + (size_t)NW * G_T * (D + 2) * 4, 16);
   p->off_final = (int)off; off = align_up(off + (size_t)G_T * (D + 2) * 4, 16);

@@ -116,7 +116,7 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 __device__ __forceinline__ void trace(const FusedParams& p, int k) {
-  if (p.trace != nullptr && threadIdx.x == 0) p.trace[(size_t)blockIdx.x * 8 + k] = globaltimer();
+  if (p.trace != nullptr && threadIdx.x == 0 && !((p.debug & 4) && k > 0)) p.trace[(size_t)blockIdx.x * 8 + k] = globaltimer();
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -237,6 +237,9 @@ __global__ void __launch_bounds__(NW * 32) fused_decode_tma_kernel(
     prefetch_desc(&vbox_map);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended row are visible
+  // the next layer's K0 may be scheduled into the tail of this grid (it stages
+  // its P, then waits for this grid to complete before reading activations)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   trace(p, 0);
 
   Ctx c;

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <math_constants.h>
 
 #include "loki_common.cuh"
@@ -38,6 +39,7 @@ struct MiscState {
   int32_t ncand[2];     // candidate list lengths (single-head fast path)
   int32_t n_union;      // rows gathered in phase 3 (single-head fast path)
   int32_t wcnt[2][32];  // per-warp counts of the ordered emission
+  long long probe[16];  // LOKI_DEBUG & 8: clock64 stamps of block 0 (tuning only)
 };
 
 // Exclusive prefix of `pred` over the block in thread order, plus the total.
@@ -74,6 +76,19 @@ __device__ __forceinline__ void merge_state(float& m, float& l, float m2, float 
   s2 = (m2 == -CUDART_INF_F) ? 0.f : exp2f(m2 - mn);
   l = l * s1 + l2 * s2;
   m = mn;
+}
+
+#define LOKI_PROBE(ms, k)                                                  \
+  do {                                                                     \
+    if ((p.debug & 8) && threadIdx.x == 0) (ms)->probe[(k)] = clock64();  \
+  } while (0)
+
+__device__ __forceinline__ void dbg_stamp(const FusedParams& p, int slot) {
+  if ((p.debug & 4) && p.trace != nullptr && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(size_t)blockIdx.x * 8 + slot] = t;
+  }
 }
 
 // Per-CTA view of its (batch, KV head) unit and cache slice.
@@ -169,6 +184,110 @@ __device__ __forceinline__ void keys_from_scores(const FusedParams& p, const Ctx
 //     no extra scan over the slice;
 //   - the ordered emission writes the phase-3 gather list and idx_out directly
 //     (two passes over warp-contiguous row ranges, one block barrier).
+// Exact end of the single-head radix select once at most 256 keys match
+// the prefix cluster-wide: every CTA publishes its candidate keys and its
+// count of keys above the prefix, one cluster barrier, then every CTA ranks
+// the (small) candidate union itself -- the threshold, the tie split and the
+// per-rank offsets follow without further barriers.
+template <int NT>
+__device__ void exact_finish(const FusedParams& p, const Ctx& c, cg::cluster_group& cluster, int shift, int level,
+                             int r0, int r1, const uint16_t* segA, const uint16_t* segB, int nA, int nB) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  MiscState* ms = c.ms;
+  const uint32_t mask = 0xFFFFFFFFu << shift;
+  const uint32_t pre = ms->prefix[0];
+  const unsigned lt = (1u << lane) - 1u;
+  const int n_src = level == 0 ? (r1 - r0) : (level == 1 ? nA : nB);
+  auto key_at = [&](int i) {
+    const int j = level == 0 ? r0 + i : (level == 1 ? (int)segA[i] : (int)segB[i]);
+    return c.keys[j];
+  };
+  // publish: candidate keys into ghist[0, n) in warp order
+  int cnt = 0;
+  for (int i0 = 0; i0 < n_src; i0 += 32) {
+    const int i = i0 + lane;
+    cnt += __popc(__ballot_sync(0xffffffffu, i < n_src && (key_at(i) & mask) == pre));
+  }
+  if (lane == 0) ms->wcnt[0][w] = cnt;
+  __syncthreads();
+  int off = 0, tot = 0;
+  for (int ww = 0; ww < NW; ++ww) {
+    off += ww < w ? ms->wcnt[0][ww] : 0;
+    tot += ms->wcnt[0][ww];
+  }
+  for (int i0 = 0; i0 < n_src; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t key = i < n_src ? key_at(i) : 0u;
+    const bool m = i < n_src && (key & mask) == pre;
+    const unsigned bal = __ballot_sync(0xffffffffu, m);
+    if (m) c.ghist[off + __popc(bal & lt)] = key;
+    off += __popc(bal);
+  }
+  if (tid == 0) ms->ncand[0] = tot;
+  cluster.sync();
+  // gather every rank's candidates (and their rank) into local scratch
+  uint32_t* ck = c.hist;                   // keys   [<= 256]
+  uint32_t* cr = c.hist + kRadixBins;      // owner  [<= 256]
+  int offs[17];
+  int ntot = 0;
+  for (int r = 0; r < c.C; ++r) {
+    offs[r] = ntot;
+    ntot += cluster.map_shared_rank(ms, r)->ncand[0];
+  }
+  offs[c.C] = ntot;
+  for (int i = tid; i < ntot; i += NT) {
+    int r = 0;
+    while (offs[r + 1] <= i) ++r;
+    ck[i] = cluster.map_shared_rank(c.ghist, r)[i - offs[r]];
+    cr[i] = (uint32_t)r;
+  }
+  if (tid < c.C) ms->wcnt[1][tid] = cluster.map_shared_rank(ms, tid)->cnt_gt[0];
+  __syncthreads();
+  // the krem-th largest candidate is the exact threshold T
+  const int krem = ms->krem[0];
+  for (int i = tid; i < ntot; i += NT) {
+    const uint32_t x = ck[i];
+    int g = 0, e = 0;
+    for (int t = 0; t < ntot; ++t) {
+      g += ck[t] > x;
+      e += ck[t] == x;
+    }
+    if (g < krem && krem <= g + e) ms->T[0] = x;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint32_t T = ms->T[0];
+    int above_T = 0;
+    for (int t = 0; t < ntot; ++t) above_T += ck[t] > T;
+    const int need = krem - above_T;  // threshold ties still to take, lowest rank first
+    int eq_before = 0, sel_before = 0, take = 0;
+    for (int r = 0; r <= c.rank; ++r) {
+      int gt_r = ms->wcnt[1][r], eq_r = 0;
+      for (int t = offs[r]; t < offs[r + 1]; ++t) {
+        gt_r += ck[t] > T;
+        eq_r += ck[t] == T;
+      }
+      int tk = need - eq_before;  // ties at T go to the lowest ranks (lowest indices) first
+      tk = tk < 0 ? 0 : (tk > eq_r ? eq_r : tk);
+      if (r < c.rank) {
+        sel_before += gt_r + tk;
+        eq_before += eq_r;
+      } else {
+        take = tk;
+        ms->lgt[0] = gt_r;
+        ms->leq[0] = eq_r;
+      }
+    }
+    ms->done[0] = 2;
+    ms->gt[0] = (long long)T;
+    ms->tie_take[0] = take;
+    ms->sel_off[0] = sel_before;
+    ms->n_union = ms->lgt[0] + take;
+  }
+  __syncthreads();
+}
+
 template <int NT>
 __device__ void select_single(const FusedParams& p, const Ctx& c, cg::cluster_group& cluster) {
   constexpr int NW = NT / 32;
@@ -176,61 +295,83 @@ __device__ void select_single(const FusedParams& p, const Ctx& c, cg::cluster_gr
   MiscState* ms = c.ms;
   const int n_local = c.n_local;
   const uint32_t* keys = c.keys;
-  uint16_t* listA = c.uni;
-  uint16_t* listB = reinterpret_cast<uint16_t*>(c.part);
-  const int capB = NW * (c.D + 2) * 2;
+  const unsigned lt = (1u << lane) - 1u;
+  // warp w owns the contiguous rows [w * Rw, w * Rw + Rw) and private segments of
+  // the candidate lists (no cross-warp atomics): listA in `uni`, listB in the merge scratch
+  const int Rw = ceil_div(ceil_div(n_local, NW), 32) * 32;
+  const int r0 = min(w * Rw, n_local), r1 = min(r0 + Rw, n_local);
+  uint16_t* segA = c.uni + w * Rw;
+  const int capBw = (NW * (c.D + 2) * 2) / NW;  // uint16 entries per warp in the merge scratch
+  uint16_t* segB = reinterpret_cast<uint16_t*>(c.part) + w * capBw;
+  int nA = 0, nB = 0;  // this warp's list lengths (warp-uniform)
+  int level = 0;       // 0: scan rows, 1: scan segA, 2: scan segB
+  bool exact = false;  // threshold found by exact_finish (counts already exchanged)
   if (tid == 0) {
-    ms->ncand[0] = 0;
-    ms->ncand[1] = 0;
-    ms->cnt_gt[0] = 0;      // running count of local keys above the prefix
-    ms->lgt[1] = n_local;   // local keys matching the prefix so far
+    ms->cnt_gt[0] = 0;     // running count of local keys above the prefix
+    ms->lgt[1] = n_local;  // local keys matching the prefix so far
   }
   __syncthreads();
-  const uint16_t* src = nullptr;  // nullptr: every key of the slice
-  int src_n = n_local;
+  LOKI_PROBE(ms, 0);
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 24 - 8 * pass;
     uint32_t* hcur = c.hist + (pass & 1) * kRadixBins;
     if (pass > 0) {
       const uint32_t hi_mask = 0xFFFFFFFFu << (shift + 8);
       const uint32_t pre = ms->prefix[0];
-      uint16_t* dst = (pass == 1) ? listA : ((pass == 2 && ms->lgt[1] <= capB) ? listB : nullptr);
-      int* dcount = (pass == 1) ? &ms->ncand[0] : &ms->ncand[1];
-      for (int i0 = 0; i0 < src_n; i0 += NT) {
-        const int i = i0 + tid;
-        const int j = i < src_n ? (src ? (int)src[i] : i) : 0;
-        const uint32_t key = i < src_n ? keys[j] : 0u;
-        const bool m = (i < src_n) && ((key & hi_mask) == pre);
-        if (m) atomicAdd(&hcur[(key >> shift) & 0xFFu], 1u);
-        if (dst != nullptr) {
-          const unsigned bal = __ballot_sync(0xffffffffu, m);
-          int base = 0;
-          if (lane == 0 && bal) base = atomicAdd(dcount, __popc(bal));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (m) dst[base + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)j;
+      // compact the keys matching the prefix: pass 1 -> segA, pass 2 -> segB when it surely fits
+      const int to = (pass == 1) ? 1 : ((pass == 2 && ms->lgt[1] <= capBw) ? 2 : 0);
+      uint16_t* dst = to == 1 ? segA : segB;
+      const int n_src = level == 0 ? (r1 - r0) : (level == 1 ? nA : nB);
+      int nd = 0;
+      constexpr int U = 4;  // independent keys in flight per lane
+      for (int i0 = 0; i0 < n_src; i0 += 32 * U) {
+        int jj[U];
+        uint32_t kk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * 32 + lane;
+          jj[u] = i < n_src ? (level == 0 ? r0 + i : (level == 1 ? (int)segA[i] : (int)segB[i])) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) kk[u] = jj[u] >= 0 ? keys[jj[u]] : 0u;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool m = jj[u] >= 0 && ((kk[u] & hi_mask) == pre);
+          if (m) atomicAdd(&hcur[(kk[u] >> shift) & 0xFFu], 1u);
+          if (to) {
+            const unsigned bal = __ballot_sync(0xffffffffu, m);
+            if (m) dst[nd + __popc(bal & lt)] = (uint16_t)jj[u];
+            nd += __popc(bal);
+          }
         }
       }
-      __syncthreads();
-      if (dst != nullptr) {
-        src = dst;
-        src_n = *dcount;
-      }
+      if (to == 1) { nA = nd; level = 1; }
+      if (to == 2) { nB = nd; level = 2; }
     }
+    LOKI_PROBE(ms, 1 + 4 * pass);
+    // cluster.sync also orders this CTA's histogram writes for every thread
     cluster.sync();
+    LOKI_PROBE(ms, 2 + 4 * pass);
+    // merge the C ranks' histograms, one bin per thread (DSMEM loads in parallel);
+    // the other buffer was last read remotely two passes ago, before this
+    // pass's cluster barrier: clear it for the next pass at the same time
     for (int i = tid; i < kRadixBins; i += NT) {
       uint32_t sum = 0;
       for (int r = 0; r < c.C; ++r) sum += cluster.map_shared_rank(hcur, r)[i];
       c.ghist[i] = sum;
+      c.hist[((pass + 1) & 1) * kRadixBins + i] = 0u;
     }
     __syncthreads();
+    LOKI_PROBE(ms, 3 + 4 * (pass & 1));
     if (w == 0 && !ms->done[0]) {
       const int krem = ms->krem[0];
       uint32_t cnt[8], lc[8];
       uint32_t lsum = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {  // lane 0 holds the top bins 255..248
-        cnt[i] = c.ghist[255 - (lane * 8 + i)];
-        lc[i] = hcur[255 - (lane * 8 + i)];
+        const int bin = 255 - (lane * 8 + i);
+        lc[i] = hcur[bin];
+        cnt[i] = c.ghist[bin];
         lsum += cnt[i];
       }
       uint32_t incl = lsum;
@@ -270,6 +411,7 @@ __device__ void select_single(const FusedParams& p, const Ctx& c, cg::cluster_gr
         const int lmatch = (int)at;
         ms->cnt_gt[0] = lgt;
         ms->lgt[1] = lmatch;  // size of the next candidate list
+        ms->ncand[1] = (int)cnt[istar];  // cluster-wide keys matching the new prefix
         if ((int)cnt[istar] == rem) {  // the whole boundary bin is in: no tie to break
           ms->done[0] = 1;
           ms->gt[0] = (long long)pre - 1;
@@ -287,18 +429,25 @@ __device__ void select_single(const FusedParams& p, const Ctx& c, cg::cluster_gr
       }
     }
     __syncthreads();
-    if (ms->done[0]) break;
-    if (pass < 3) {
-      uint32_t* hnext = c.hist + ((pass + 1) & 1) * kRadixBins;
-      for (int i = tid; i < kRadixBins; i += NT) hnext[i] = 0u;
-      __syncthreads();
+    LOKI_PROBE(ms, 4 + 4 * (pass & 1));
+    if (!ms->done[0] && ms->ncand[1] <= kRadixBins) {
+      // few candidates left cluster-wide: finish exactly from the candidate keys
+      exact_finish<NT>(p, c, cluster, shift, level, r0, r1, segA, segB, nA, nB);
+      exact = true;
+      break;
     }
+    if (pass == 0) dbg_stamp(p, 1);
+    if (pass == 1) dbg_stamp(p, 4);
+    if (pass == 2) dbg_stamp(p, 5);
+    if (pass == 3) dbg_stamp(p, 6);
+    if (ms->done[0]) break;
   }
-  if (p.trace != nullptr && tid == 0) {
+  if (p.trace != nullptr && tid == 0 && !(p.debug & 4)) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[(size_t)blockIdx.x * 8 + 2] = t;
   }
+  if (!exact) {
   cluster.sync();  // every CTA's counts visible
   if (tid == 0) {
     const int need = ms->krem[0];
@@ -319,26 +468,34 @@ __device__ void select_single(const FusedParams& p, const Ctx& c, cg::cluster_gr
     ms->n_union = ms->lgt[0] + take;
   }
   __syncthreads();
-  if (p.trace != nullptr && tid == 0) {
+  }
+  if (p.trace != nullptr && tid == 0 && !(p.debug & 4)) {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.trace[(size_t)blockIdx.x * 8 + 3] = t;
   }
+  dbg_stamp(p, 7);
 
-  // ordered emission: warp w owns rows [w * Rw, (w + 1) * Rw)
+  LOKI_PROBE(ms, 9);
+  // ordered emission over the warp's rows, four keys per lane per step
   const long long gt = ms->gt[0];
   const uint32_t Tk = ms->T[0];
   const int take = ms->tie_take[0];
   const bool ties = ms->done[0] == 2 && take > 0;
-  const int Rw = ceil_div(ceil_div(n_local, NW), 32) * 32;
-  const int r0 = min(w * Rw, n_local), r1 = min(r0 + Rw, n_local);
+  const bool partial = ties && take < ms->leq[0];  // only then do tie ranks matter
   int cg_ = 0, ct = 0;
-  for (int j0 = r0; j0 < r1; j0 += 32) {
-    const int j = j0 + lane;
-    const uint32_t key = j < r1 ? keys[j] : 0u;
-    cg_ += __popc(__ballot_sync(0xffffffffu, j < r1 && (long long)key > gt));
-    ct += __popc(__ballot_sync(0xffffffffu, j < r1 && ties && key == Tk));
+  for (int j0 = r0; j0 < r1; j0 += 128) {
+    const int jb = j0 + 4 * lane;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = jb + e;
+      const uint32_t key = j < r1 ? keys[j] : 0u;
+      cg_ += (j < r1 && (long long)key > gt);
+      ct += (j < r1 && ties && key == Tk);
+    }
   }
+  cg_ = __reduce_add_sync(0xffffffffu, cg_);
+  ct = __reduce_add_sync(0xffffffffu, ct);
   if (lane == 0) {
     ms->wcnt[0][w] = cg_;
     ms->wcnt[1][w] = ct;
@@ -353,25 +510,71 @@ __device__ void select_single(const FusedParams& p, const Ctx& c, cg::cluster_gr
     tseen += tw;
   }
   int32_t* dsti = p.idx_out ? p.idx_out + c.qrow0 * p.idx_stride + ms->sel_off[0] : nullptr;
-  const unsigned lt = (1u << lane) - 1u;
-  for (int j0 = r0; j0 < r1; j0 += 32) {
-    const int j = j0 + lane;
-    const uint32_t key = j < r1 ? keys[j] : 0u;
-    const bool g1 = j < r1 && (long long)key > gt;
-    const bool t1 = j < r1 && ties && key == Tk;
-    const unsigned tb = __ballot_sync(0xffffffffu, t1);
-    const bool sel = g1 || (t1 && tseen + __popc(tb & lt) < take);
-    const unsigned sb = __ballot_sync(0xffffffffu, sel);
-    if (sel) {
-      const int q = pos + __popc(sb & lt);
-      c.uni[q] = (uint16_t)j;
-      c.selmask[j] = 1;  // phase-3 head mask and the weights emission
-      if (dsti) dsti[q] = c.s0 + j;
+  for (int j0 = r0; j0 < r1; j0 += 128) {
+    const int jb = j0 + 4 * lane;
+    bool g1[4], t1[4];
+    int nt = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = jb + e;
+      const uint32_t key = j < r1 ? keys[j] : 0u;
+      g1[e] = j < r1 && (long long)key > gt;
+      t1[e] = j < r1 && ties && key == Tk;
+      nt += t1[e];
     }
-    pos += __popc(sb);
-    tseen += __popc(tb);
+    bool sel[4];
+    int ns = 0, tin = 0;
+    if (partial) {
+      // ties before this lane's first key, in row order
+      tin = nt;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, tin, off);
+        if (lane >= off) tin += t;
+      }
+      int trank = tseen + tin - nt;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        sel[e] = g1[e] || (t1[e] && trank < take);
+        trank += t1[e];
+        ns += sel[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        sel[e] = g1[e] || t1[e];
+        ns += sel[e];
+      }
+    }
+    int sin = ns;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, sin, off);
+      if (lane >= off) sin += t;
+    }
+    int q = pos + sin - ns;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (sel[e]) {
+        const int j = jb + e;
+        c.uni[q] = (uint16_t)j;
+        c.selmask[j] = 1;  // phase-3 head mask and the weights emission
+        if (dsti) dsti[q] = c.s0 + j;
+        ++q;
+      }
+    }
+    pos += __shfl_sync(0xffffffffu, sin, 31);
+    if (partial) tseen += __shfl_sync(0xffffffffu, tin, 31);
   }
   __syncthreads();
+  LOKI_PROBE(ms, 10);
+  if ((p.debug & 8) && threadIdx.x == 0 && blockIdx.x == 0) {
+    printf("loki select probe (cycles from start): scan1 %lld | p0: sync %lld merge %lld dec %lld | p1: scan %lld sync %lld merge %lld dec %lld | exact %lld emit %lld | cand %d\n",
+           ms->probe[1] - ms->probe[0], ms->probe[2] - ms->probe[1], ms->probe[3] - ms->probe[2],
+           ms->probe[4] - ms->probe[3], ms->probe[5] - ms->probe[4], ms->probe[6] - ms->probe[5],
+           ms->probe[7] - ms->probe[6], ms->probe[8] - ms->probe[7], ms->probe[9] - ms->probe[8],
+           ms->probe[10] - ms->probe[9], ms->ncand[1]);
+  }
 }
 
 // Phase 2: cluster-wide MSB radix select of each head's k_b largest keys
