@@ -124,7 +124,7 @@ class DecodeCall:
         _lib.check(self.lib.loki_decode_workspace_bytes(ctypes.byref(a), ctypes.byref(nbytes)))
         self.workspace = None
         if nbytes.value:
-            self.workspace = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
+            self.workspace = torch.zeros(nbytes.value, dtype=torch.uint8, device=self.device)
             a.workspace = self.workspace.data_ptr()
             a.workspace_bytes = nbytes.value
         self.args = a

@@ -116,7 +116,7 @@ struct TmaGeom {
 
 // TMA plan pieces for (dtype, D, d, G_T); false when the layout is outside
 // what the TMA kernel handles.
-bool tma_geom(const loki_decode_args* a, int G_T, TmaGeom* t) {
+bool tma_geom(const loki_decode_args* a, int G_T, TmaGeom* t, int stage_bytes = 0) {
   const loki_kv_geom& g = a->g;
   const int e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   const int vec = g.dtype == LOKI_DTYPE_BF16 ? (G_T == 8 ? 4 : 8) : 4;
@@ -128,7 +128,7 @@ bool tma_geom(const loki_decode_args* a, int G_T, TmaGeom* t) {
   // a stage is digested by one warp: phase 1 in passes of 4 x rpw1 rows,
   // phase 3 in passes of 2 x rpw3 rows; gather4 needs multiples of 4 rows
   const int rpw1 = 32 / loki::next_pow2(dbox / vec);
-  const int kStageBytes = stage_bytes_cfg();
+  const int kStageBytes = stage_bytes > 0 ? stage_bytes : stage_bytes_cfg();
   int r1 = kStageBytes / (dbox * e);
   if (r1 > 256) r1 = 256;
   r1 = r1 / (4 * rpw1) * (4 * rpw1);
@@ -231,6 +231,133 @@ loki_status make_plan(const loki_decode_args* a, loki::Plan* plan, loki::FusedPa
   return LOKI_OK;
 }
 
+
+// ---------------------------------------------------------------- pipelined plan
+struct PipePlan {
+  loki::PipeParams p{};
+  TmaGeom tg{};
+  int G_T = 1;
+  int grid = 0;
+  size_t smem = 0;
+  size_t ws = 0;
+  size_t off_hist = 0, off_keys = 0, off_tcs = 0, off_poff = 0, off_part = 0, off_logits = 0;
+};
+
+// The persistent pipelined kernel (loki_pipe.cu) serves the attending TOPK
+// path whenever the cache is TMA-addressable; false -> cluster kernels.
+bool pipe_eligible(const loki_decode_args* a) {
+  const loki_kv_geom& g = a->g;
+  const int G_T = loki::next_pow2(g.Hq / g.Hkv);
+  const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
+  const bool contiguous = (g.Hkv == 1 || g.stride_h == (int64_t)g.S_cap * g.stride_s) &&
+                          (g.B == 1 || g.stride_b == (int64_t)g.Hkv * g.S_cap * g.stride_s);
+  return env_int("LOKI_PIPE", 1) != 0 && a->select_mode == LOKI_SELECT_TOPK && a->ext_scores == nullptr &&
+         a->out != nullptr && a->K != nullptr && a->V != nullptr && contiguous && aligned(a->K, 16) &&
+         aligned(a->V, 16) && (g.stride_s * e) % 16 == 0 && (long long)g.B * g.Hkv * g.S_cap < (1LL << 31) &&
+         a->S_max < (1 << 24) && loki::pipe_supported(g.dtype, g.D, G_T) && a->cluster_override == 0;
+}
+
+loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
+  const loki_kv_geom& g = a->g;
+  const int G = g.Hq / g.Hkv;
+  const int G_T = loki::next_pow2(G);
+  const int units = g.B * g.Hkv;
+  const int e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
+  pl->G_T = G_T;
+  const int stage = env_int("LOKI_PIPE_STAGE_KB", 4) * 1024;
+  if (!tma_geom(a, G_T, &pl->tg, stage)) return fail(LOKI_ERR_UNSUPPORTED, "pipe: TMA geometry");
+  loki::PipeParams& p = pl->p;
+  p.nst = env_int("LOKI_PIPE_STAGES", 2);
+  p.stage_bytes = stage;
+  p.r1 = pl->tg.r1;
+  p.dbox = pl->tg.dbox;
+  p.r3 = pl->tg.r3;
+  p.hbits = G_T <= 2 ? 11 : (G_T == 4 ? 10 : 9);
+  const int d = a->d < 1 ? 1 : a->d;
+  const int vec = pl->tg.vec;
+  p.split_k = env_int("LOKI_SPLITK", 1) != 0 && d < g.D && d % vec == 0 && ((g.D - d) * e) % 32 == 0;
+  // chunk = part: kNB 128-row blocks per warp in the B-item row scan (loki_pipe.cu)
+  const int kNB = G_T >= 4 ? 1 : 4 / G_T;
+  const int Lc = kNB * 128 * loki::pipe_warps();
+  if (Lc % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", Lc, p.r1);
+  p.Lc = Lc;
+  p.nA = loki::ceil_div(a->S_max, Lc);
+  p.units = units;
+  pl->smem = loki::pipe_layout(G_T, &p);
+  const size_t ring = (size_t)loki::pipe_warps() * p.nst * p.stage_bytes;
+  if ((size_t)loki::pipe_warps() * G_T * (g.D + 2) * 4 > ring || p.cand_cap < 256)
+    return fail(LOKI_ERR_UNSUPPORTED, "pipe: ring of %zu bytes too small", ring);
+  if (pl->smem > kSmemMax) return fail(LOKI_ERR_UNSUPPORTED, "pipe: shared memory plan %zu bytes", pl->smem);
+  const int occ = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem);
+  if (occ < 1) return fail(LOKI_ERR_UNSUPPORTED, "pipe: kernel does not fit on an SM (%zu B smem)", pl->smem);
+  const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
+  pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
+  const double lagx = env_int("LOKI_PIPE_LAG_X10", 25) / 10.0;
+  int lag = (int)ceil(lagx * pl->grid / (double)(2 * p.nA));
+  p.lag = lag < 1 ? 1 : (lag > units ? units : lag);
+  p.n_tickets = (long long)(units + p.lag) * (2 * p.nA);
+  // workspace: ctrl | hist | keys | sel | part | logits
+  const int HB = 1 << p.hbits;
+  size_t off = loki::align_up((size_t)(2 + 4 * (size_t)units) * 4, 256);
+  pl->off_hist = off;
+  off = loki::align_up(off + (size_t)units * G * HB * 4, 256);
+  pl->off_keys = off;
+  p.kstride = loki::ceil_div(g.S_cap, 4) * 4;
+  off = loki::align_up(off + (size_t)units * G * p.kstride * 4, 256);
+  pl->off_tcs = off;
+  off = loki::align_up(off + (size_t)units * G * 8, 256);
+  pl->off_poff = off;
+  if (a->idx_out != nullptr) off = loki::align_up(off + (size_t)units * G * p.nA * 4, 256);
+  pl->off_part = off;
+  off = loki::align_up(off + (size_t)units * p.nA * G * (g.D + 2) * 4, 256);
+  pl->off_logits = off;
+  if (a->weights_out != nullptr) off = loki::align_up(off + (size_t)units * G * g.S_cap * 4, 256);
+  pl->ws = off;
+  return LOKI_OK;
+}
+
+loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
+  const loki_kv_geom& g = a->g;
+  if (a->workspace == nullptr || a->workspace_bytes < pl.ws)
+    return fail(LOKI_ERR_SHAPE, "workspace of %zu bytes required", pl.ws);
+  loki::PipeParams& p = pl.p;
+  uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+  p.q_hat = a->q_hat;
+  p.B = g.B;
+  p.Hq = g.Hq;
+  p.Hkv = g.Hkv;
+  p.G = g.Hq / g.Hkv;
+  p.D = g.D;
+  p.S_cap = g.S_cap;
+  p.lens = a->lens;
+  p.d = a->d < 1 ? 1 : a->d;
+  p.k_f = a->k_f;
+  p.k_fixed = a->k_fixed;
+  p.idx_stride = a->idx_stride;
+  p.out = a->out;
+  p.idx_out = a->idx_out;
+  p.approx_out = a->approx_out;
+  p.weights_out = a->weights_out;
+  p.qscale = (float)(1.4426950408889634 / sqrt((double)g.D));
+  p.unit_rows = g.S_cap;
+  p.ctrl = reinterpret_cast<uint32_t*>(ws);
+  p.hist = reinterpret_cast<uint32_t*>(ws + pl.off_hist);
+  p.keys = reinterpret_cast<uint32_t*>(ws + pl.off_keys);
+  p.tcs = reinterpret_cast<unsigned long long*>(ws + pl.off_tcs);
+  p.poff = a->idx_out ? reinterpret_cast<uint32_t*>(ws + pl.off_poff) : nullptr;
+  p.part = reinterpret_cast<float*>(ws + pl.off_part);
+  p.logits = a->weights_out ? reinterpret_cast<float*>(ws + pl.off_logits) : nullptr;
+  p.debug = env_int("LOKI_DEBUG", 0);
+  p.trace = (loki::g_phase_trace != nullptr && p.n_tickets * 4 <= (long long)loki::g_phase_trace_ctas * 8)
+                ? loki::g_phase_trace : nullptr;
+  loki::TmaDesc maps[3];
+  if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, maps))
+    return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
+  cudaError_t e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return cuda_status(e, "loki_decode (pipe) launch");
+}
+
 }  // namespace
 
 extern "C" {
@@ -252,6 +379,13 @@ loki_status loki_device_check(int32_t device) {
 loki_status loki_decode_workspace_bytes(const loki_decode_args* a, size_t* bytes) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
+  {
+    PipePlan pl;
+    if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {
+      *bytes = pl.ws;
+      return LOKI_OK;
+    }
+  }
   loki::Plan plan;
   loki::FusedParams p{};
   TmaGeom tg{};
@@ -265,6 +399,13 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
                              size_t* smem_bytes) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
+  PipePlan pl;
+  if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {  // persistent grid: 0 CTAs per unit
+    if (ctas_per_unit) *ctas_per_unit = 0;
+    if (rows_per_cta) *rows_per_cta = pl.p.Lc;
+    if (smem_bytes) *smem_bytes = pl.smem;
+    return LOKI_OK;
+  }
   loki::Plan plan;
   loki::FusedParams p{};
   TmaGeom tg{};
@@ -279,6 +420,10 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
 loki_status loki_decode(const loki_decode_args* a, void* stream) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
+  {
+    PipePlan pl;
+    if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) return run_pipe(a, pl, stream);
+  }
   loki::Plan plan;
   loki::FusedParams p{};
   TmaGeom tg{};

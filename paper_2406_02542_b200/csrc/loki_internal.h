@@ -43,6 +43,47 @@ struct FusedParams {
   int debug;                 // LOKI_DEBUG bits (tuning experiments only): 1 = dense rows via gather4
 };
 
+// Persistent pipelined decode (loki_pipe.cu): a grid of resident CTAs draws
+// tickets from one global counter; ticket -> work item
+//   A(u, c)  phase 1 of chunk c of unit u (approx scores -> keys, histogram);
+//            the last A arriver of a unit runs its top-k selection
+//   B(u, q)  phase 3 over rows [q * Lc, (q + 1) * Lc) of unit u: picks its
+//            selected rows from the keys and the published thresholds, gathers
+//            them, online softmax -> partial state; the last B arriver merges.
+// B(u, *) tickets come `lag` units after A(u, *), so other CTAs keep HBM busy
+// while a unit's selection runs.  The workspace must be zero on first use;
+// every launch leaves it zero again (counters / histograms self-reset).
+struct PipeParams {
+  const float* q_hat;  // [B, Hq, D]
+  int B, Hq, Hkv, G, D, S_cap;
+  const int32_t* lens;
+  int d;
+  double k_f;
+  int k_fixed;
+  int64_t idx_stride;
+  float* out;
+  int32_t* idx_out;
+  float* approx_out;
+  float* weights_out;
+  float qscale;  // log2(e) / sqrt(D)
+  int nst, stage_bytes, off_ring, off_bars, off_hist, off_ents;
+  int r1, dbox, r3;
+  long long unit_rows;
+  int units, Lc, nA, lag, hbits, cand_cap;
+  long long n_tickets;
+  int split_k;       // 1: phase 3 gathers K columns [d, D) only and reuses the phase-1 partial score
+  uint32_t* ctrl;    // [2 + 4 * units]: ticket, exits, then per unit {A arrivals, B arrivals, ready, -}
+  uint32_t* hist;    // [units][G][1 << hbits]
+  uint32_t* keys;    // [units][G][kstride] order keys of the approx scores
+  int kstride;       // S_cap rounded up to a multiple of 4 (uint4 scans)
+  unsigned long long* tcs;  // [units][G] selection thresholds on composite keys
+  uint32_t* poff;    // [units][G][nA] idx_out offset of each part (idx_out only)
+  float* part;       // [units][nA][G][D + 2] per-part (acc[D], m, l)
+  float* logits;     // [units][G][S_cap] exact logits (weights_out only) or null
+  long long* trace;  // optional [n_tickets][4] {start, end, sm | kind << 16 | block << 32, tail start}
+  int debug;
+};
+
 // Phase-trace buffer installed by loki_set_phase_trace (diagnostics only).
 extern long long* g_phase_trace;
 extern int g_phase_trace_ctas;
@@ -95,5 +136,15 @@ cudaError_t launch_softmax_rows(const float* x, int64_t rows, int n, int64_t str
 cudaError_t launch_rope(const void* x, void* out, int io_dtype, int64_t n_rows, int D,
                         const int64_t* positions, const double* inv_freq, cudaStream_t st);
 cudaError_t launch_index_status(const int64_t* idx, int n, int64_t bound, int32_t* status, cudaStream_t st);
+
+// persistent pipelined decode (loki_pipe.cu)
+size_t pipe_layout(int G_T, PipeParams* p);
+bool pipe_supported(int dtype, int D, int G_T);
+// lead boxes {dbox, r1} (64 B promotion), K row gathers of columns [kcol0, D), V row gathers
+bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, int r1, int kcol0, TmaDesc* maps);
+cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
+                        cudaStream_t st);
+int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem);
+int pipe_warps();
 
 }  // namespace loki

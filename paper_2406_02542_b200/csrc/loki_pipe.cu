@@ -1,0 +1,1031 @@
+// Persistent, dynamically scheduled Loki decode attention -- the TOPK hot
+// path on sm_100a (attention.py:166-185 loki_rank_and_attend, batched).
+//
+// Why not one cluster per (batch, KV head) unit (loki_decode_tma.cu): there
+// every resident CTA runs phase 1 -> selection -> phase 3 -> merge in
+// lockstep, so HBM idles while the whole GPU selects (profiles/r01_summary.md:
+// 53 % of the roofline).  Here a grid of resident CTAs draws tickets from one
+// global counter and each ticket is a work item:
+//
+//   A(u, c)  phase 1 over chunk c of unit u: TMA boxes of the leading d
+//            columns (L2 promotion 64 B: exactly d*S*e DRAM bytes), approx
+//            scores (kernels.py:223-241) -> order keys in an L2-resident
+//            workspace + a (1 << hbits)-bin histogram of their top bits.  The
+//            LAST A arriver of the unit runs the unit's top-k selection
+//            (linalg.py:95-118) and publishes the ascending union list.
+//   B(u, q)  phase 3 over part q of that list: tile::gather4 of the selected
+//            K and V rows, exact logits / sqrt(D), online softmax and V
+//            accumulation (kernels.py:244-279, linalg.py:76-92) -> a partial
+//            (m, l, acc) state.  The LAST B arriver merges the parts in fixed
+//            order and writes the output row.
+//
+// B tickets of unit u are issued `lag` units after its A tickets, so while
+// one CTA selects, the others keep streaming.  Items are 256 KB - 1 MB of HBM
+// traffic, so the tail of the grid is short and there is no wave
+// quantisation.  Everything is deterministic: selections are exact, partial
+// states are merged in fixed order (warps, then parts).
+//
+// Selection on 64-bit composite keys (order_key(score) << 32 | ~row): all
+// composites are distinct and "the k largest composites" is exactly the
+// reference's rule -- every score above the threshold, then threshold ties
+// lowest row first.  MSB radix select: the first digit comes from the
+// histogram built during phase 1; further digits are resolved over the
+// candidates (compacted to shared memory once they fit).
+#include <cuda.h>
+
+#include "loki_fused.cuh"
+#include "loki_tma.cuh"
+
+namespace loki {
+
+namespace {
+
+using namespace tma;
+using fused::kMaxG;
+using fused::merge_state;
+
+#ifndef LOKI_PIPE_WARPS
+#define LOKI_PIPE_WARPS 8
+#endif
+constexpr int kPW = LOKI_PIPE_WARPS;  // warps per CTA; every warp streams through its own TMA ring
+constexpr int kPT = kPW * 32;
+
+struct PipeShared {
+  unsigned next_ticket;
+  int last;
+  long long t_sel;
+  int fb_bin;
+  unsigned fb_above, fb_cnt;
+  int scan[kPW];
+  int ncand, ncand_first;
+  unsigned long long tsel;
+  unsigned long long Tc[kMaxG];
+  int wcnt[kPW][kMaxG + 1];
+  float gm[kMaxG], gl[kMaxG];
+};
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// generic-proxy shared-memory writes ordered before later TMA (async-proxy) writes
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long comp_key(uint32_t key, int j) {
+  return ((unsigned long long)key << 32) | (unsigned long long)(~(uint32_t)j);
+}
+
+__device__ __forceinline__ int k_of(const PipeParams& p, int S) {
+  if (S <= 0) return 0;
+  return p.k_fixed > 0 ? (p.k_fixed < S ? p.k_fixed : S) : resolve_fraction(p.k_f, S);
+}
+
+// Block-wide inclusive scan of one value per thread, in thread order.
+__device__ __forceinline__ unsigned block_incl_scan(unsigned v, PipeShared& sh, unsigned* total) {
+  const int lane = lane_id(), w = warp_id();
+  unsigned x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += t;
+  }
+  if (lane == 31) sh.scan[w] = (int)x;
+  __syncthreads();
+  unsigned before = 0, tot = 0;
+#pragma unroll
+  for (int i = 0; i < kPW; ++i) {
+    const unsigned c = (unsigned)sh.scan[i];
+    before += i < w ? c : 0u;
+    tot += c;
+  }
+  __syncthreads();
+  *total = tot;
+  return before + x;
+}
+
+// The bin holding the need-th largest element: largest b with
+// sum_{i>b} h[i] < need <= sum_{i>=b} h[i] -> sh.fb_bin / fb_above / fb_cnt.
+__device__ void find_bin(const uint32_t* h, int nbins, unsigned need, PipeShared& sh) {
+  const int tid = threadIdx.x;
+  const int per = nbins > kPT ? nbins / kPT : 1;  // nbins is a power of two
+  const int hi = nbins - tid * per;                // this thread owns bins [hi - per, hi)
+  unsigned s = 0;
+  if (hi > 0)
+    for (int i = 0; i < per; ++i) s += h[hi - 1 - i];
+  unsigned tot;
+  const unsigned incl = block_incl_scan(s, sh, &tot);
+  const unsigned excl = incl - s;
+  if (hi > 0 && excl < need && need <= incl) {
+    unsigned acc = excl;
+    for (int i = 0; i < per; ++i) {
+      const int b = hi - 1 - i;
+      if (acc + h[b] >= need) {
+        sh.fb_bin = b;
+        sh.fb_above = acc;
+        sh.fb_cnt = h[b];
+        break;
+      }
+      acc += h[b];
+    }
+  }
+  __syncthreads();
+}
+
+// Warp-aggregated append of `c` to dst when `m` (order within dst is irrelevant).
+__device__ __forceinline__ void append_if(bool m, unsigned long long c, unsigned long long* dst, int* counter) {
+  const int lane = lane_id();
+  const unsigned bal = __ballot_sync(0xffffffffu, m);
+  int base = 0;
+  if (lane == 0 && bal) base = atomicAdd(counter, __popc(bal));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (m) dst[base + __popc(bal & ((1u << lane) - 1u))] = c;
+}
+
+// ------------------------------------------------------------------ selection
+// Scans over a unit's keys are latency-bound L2 reads: every lane keeps
+// kSU uint4 loads (16 rows) in flight.  Warp w owns the contiguous rows
+// [ra, rb) (128-row aligned) so the emission can be ordered.
+constexpr int kSU = 4;
+
+__device__ __forceinline__ uint4 ld_keys4(const uint32_t* k, int j) {
+  return __ldcg(reinterpret_cast<const uint4*>(k + j));
+}
+__device__ __forceinline__ uint32_t u4_at(const uint4& v, int e) {
+  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+}
+
+// f(jb, kk): lane's rows jb..jb+3 (caller masks rows >= rb); warp-uniform calls.
+template <typename F>
+__device__ __forceinline__ void scan_rows(const uint32_t* keys, int ra, int rb, F&& f) {
+  const int lane = lane_id();
+  for (int j0 = ra; j0 < rb; j0 += 128 * kSU) {
+    uint4 kk[kSU];
+#pragma unroll
+    for (int u = 0; u < kSU; ++u) {
+      const int jb = j0 + 128 * u + 4 * lane;
+      kk[u] = jb < rb ? ld_keys4(keys, jb) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kSU; ++u) f(j0 + 128 * u + 4 * lane, kk[u]);
+  }
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int* total) {
+  const int lane = lane_id();
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += t;
+  }
+  *total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+// Threshold of each head's top-k in unit u on 64-bit composite keys: the
+// last A arriver reads the level-0 histogram, compacts the boundary-bin rows
+// into shared memory with one L2 scan (further histogram levels only if they
+// do not fit), narrows them (radix passes, then a direct rank once <= 256
+// remain) and publishes tcs[u][g].  With idx_out it also publishes each
+// part's output offset (rows above the boundary per part + candidates kept).
+template <int G_T>
+__device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem, uint32_t* hist, PipeShared& sh) {
+  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const int G = p.G, hb = p.hbits, HB = 1 << hb;
+  uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
+  const int kb = k_of(p, S);
+  const int cap = p.cand_cap;
+  const bool offsets = p.idx_out != nullptr;
+  unsigned long long* candA = reinterpret_cast<unsigned long long*>(cand_mem);
+  unsigned long long* candB = candA + cap;
+  unsigned long long* candC = candB + cap;
+  const int Rw = ceil_div(ceil_div(S > 0 ? S : 1, kPW), 128) * 128;
+  const int ra = min(w * Rw, S), rb = min(ra + Rw, S);
+  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
+  for (int g = 0; g < G; ++g) {
+    const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
+    uint32_t* gh = p.hist + ((size_t)u * G + g) * HB;
+    uint32_t* poff = offsets ? p.poff + ((size_t)u * G + g) * p.nA : nullptr;
+    for (int i = tid; i < HB; i += kPT) {
+      hist[i] = __ldcg(&gh[i]);
+      gh[i] = 0u;  // ready for the next launch
+    }
+    if (offsets)
+      for (int q = tid; q < nparts; q += kPT) poff[q] = 0u;
+    __syncthreads();
+    if (kb == 0) {
+      if (tid == 0) p.tcs[(size_t)u * G + g] = ~0ull;
+      continue;
+    }
+    find_bin(hist, HB, (unsigned)kb, sh);
+    unsigned long long P = (unsigned long long)sh.fb_bin;
+    int nb = hb;
+    unsigned need = (unsigned)kb - sh.fb_above, cnt = sh.fb_cnt;
+    int ncand = 0;
+    bool listed = false;
+    for (;;) {
+      if (cnt <= (unsigned)cap) {  // compact the rows matching P (and count the rows above P per part)
+        if (tid == 0) sh.ncand = 0;
+        __syncthreads();
+        const unsigned long long Pc = P;
+        const int sh64 = 64 - nb;
+        scan_rows(keys, ra, rb, [&](int jb, const uint4& kk) {
+          int above = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = jb + e;
+            const unsigned long long c = comp_key(u4_at(kk, e), j);
+            const bool ok = j < rb;
+            above += (ok && (c >> sh64) > Pc) ? 1 : 0;
+            append_if(ok && (c >> sh64) == Pc, c, candA, &sh.ncand);
+          }
+          if (offsets) {  // a 128-row block lies inside one part (Lc % 128 == 0)
+            above = __reduce_add_sync(0xffffffffu, above);
+            const int j0 = __shfl_sync(0xffffffffu, jb, 0);
+            if (lane == 0 && above) atomicAdd(&poff[j0 / p.Lc], (uint32_t)above);
+          }
+        });
+        __syncthreads();
+        ncand = sh.ncand;
+        if (tid == 0) sh.ncand_first = ncand;
+        listed = true;
+        break;
+      }
+      if (cnt == need) break;
+      // one more histogram level over every row matching P
+      const int bits = min(hb, 64 - nb);
+      for (int i = tid; i < (1 << bits); i += kPT) hist[i] = 0u;
+      __syncthreads();
+      const unsigned long long Pc = P;
+      const int sh64 = 64 - nb;
+      scan_rows(keys, ra, rb, [&](int jb, const uint4& kk) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = jb + e;
+          const unsigned long long c = comp_key(u4_at(kk, e), j);
+          if (j < rb && (c >> sh64) == Pc) atomicAdd(&hist[(c >> (sh64 - bits)) & ((1ull << bits) - 1)], 1u);
+        }
+      });
+      __syncthreads();
+      find_bin(hist, 1 << bits, need, sh);
+      P = (P << bits) | (unsigned long long)sh.fb_bin;
+      nb += bits;
+      need -= sh.fb_above;
+      cnt = sh.fb_cnt;
+    }
+    unsigned long long Tc;
+    if (listed) {  // narrow inside shared memory; candA stays intact for the part counts
+      const unsigned long long* src = candA;
+      unsigned long long* dst = candB;
+      while (cnt != need && ncand > 256) {
+        const int bits = min(8, 64 - nb);
+        for (int i = tid; i < (1 << bits); i += kPT) hist[i] = 0u;
+        __syncthreads();
+        for (int i = tid; i < ncand; i += kPT)
+          atomicAdd(&hist[(src[i] >> (64 - nb - bits)) & ((1ull << bits) - 1)], 1u);
+        __syncthreads();
+        find_bin(hist, 1 << bits, need, sh);
+        P = (P << bits) | (unsigned long long)sh.fb_bin;
+        nb += bits;
+        need -= sh.fb_above;
+        cnt = sh.fb_cnt;
+        if (cnt == need) break;
+        if (tid == 0) sh.ncand = 0;
+        __syncthreads();
+        for (int i0 = 0; i0 < ncand; i0 += kPT) {
+          const int i = i0 + tid;
+          const unsigned long long c = i < ncand ? src[i] : 0ull;
+          append_if(i < ncand && (c >> (64 - nb)) == P, c, dst, &sh.ncand);
+        }
+        __syncthreads();
+        ncand = sh.ncand;
+        src = dst;
+        dst = (dst == candB) ? candC : candB;
+      }
+      if (cnt == need) {
+        Tc = nb >= 64 ? P : (P << (64 - nb));
+      } else {  // <= 256 distinct candidates: the need-th largest by direct rank
+        if (tid < ncand) {
+          const unsigned long long c = src[tid];
+          unsigned rank = 0;
+          for (int i = 0; i < ncand; ++i) rank += src[i] > c;
+          if (rank == need - 1) sh.tsel = c;
+        }
+        __syncthreads();
+        Tc = sh.tsel;
+      }
+      if (offsets) {  // kept candidates per part
+        const int n0 = sh.ncand_first;
+        for (int i = tid; i < n0; i += kPT) {
+          const unsigned long long c = candA[i];
+          if (c >= Tc) atomicAdd(&poff[(int)(~(uint32_t)c) / p.Lc], 1u);
+        }
+      }
+    } else {
+      Tc = nb >= 64 ? P : (P << (64 - nb));
+      if (offsets)  // counting pass: rows >= Tc per part
+        scan_rows(keys, ra, rb, [&](int jb, const uint4& kk) {
+          int c = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) c += (jb + e < rb && comp_key(u4_at(kk, e), jb + e) >= Tc) ? 1 : 0;
+          c = __reduce_add_sync(0xffffffffu, c);
+          const int j0 = __shfl_sync(0xffffffffu, jb, 0);
+          if (lane == 0 && c) atomicAdd(&poff[j0 / p.Lc], (uint32_t)c);
+        });
+    }
+    if (tid == 0) p.tcs[(size_t)u * G + g] = Tc;
+    if (offsets) {  // counts -> exclusive offsets (one warp)
+      __syncthreads();
+      if (w == 0) {
+        unsigned run = 0;
+        for (int q0 = 0; q0 < nparts; q0 += 32) {
+          const int q = q0 + lane;
+          const unsigned v = q < nparts ? __ldcg(&poff[q]) : 0u;
+          unsigned x = v;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += t;
+          }
+          if (q < nparts) poff[q] = run + x - v;
+          run += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) cu[0] = 0u;  // A arrivals: ready for the next launch
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release(&cu[2], 1u);
+}
+
+// ------------------------------------------------------------------ item A
+template <typename T, int G_T, int VEC, int LPR1>
+__device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t* tile, int rows_here,
+                                             const float (&q1)[G_T][VEC], int G, uint32_t* keys0, float* approx0,
+                                             uint32_t* hist, int HB, int hshift) {
+  constexpr int E = sizeof(T);
+  constexpr int RPW1 = 32 / LPR1;
+  constexpr int U = 4;  // independent rows in flight per lane
+  const int lane = lane_id();
+  const int row_bytes = p.dbox * E;
+  const int nch1 = p.dbox / VEC;
+  const int r = lane / LPR1, sl = lane % LPR1;
+  const bool lane_on = sl < nch1;
+  const int passes = p.r1 / RPW1;  // host: r1 % (U * RPW1) == 0
+  for (int ps = 0; ps < passes; ps += U) {
+    float x[U][VEC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int rr = (ps + u) * RPW1 + r;
+      if (lane_on) lds_chunk<T, VEC>(tile + rr * row_bytes + sl * VEC * E, x[u]);
+      else
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) x[u][v] = 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < G_T; ++g) {
+      float acc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u] = 0.f;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[u] = fmaf(q1[g][v], x[u][v], acc[u]);
+        acc[u] = sum_lanes<LPR1>(acc[u]);
+      }
+      if (g < G) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int rr = (ps + u) * RPW1 + r;
+          if (sl == 0 && rr < rows_here) {
+            const uint32_t key = order_key(acc[u]);
+            keys0[(size_t)g * p.kstride + rr] = key;
+            if (approx0 != nullptr) approx0[(size_t)g * p.S_cap + rr] = acc[u];
+            atomicAdd(&hist[g * HB + (key >> hshift)], 1u);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int G_T, int VEC>
+__device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, int c, uint8_t* ring,
+                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, RingPos& rp, PipeShared& sh) {
+  constexpr int E = sizeof(T);
+  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const int nsw = p.nst, SB = p.stage_bytes;
+  const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G;
+  int S = p.lens[b];
+  S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
+  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
+  if (c >= nparts) return 0;  // past this unit's length: not an arrival
+  const int row0 = c * p.Lc;
+  const int n = max(0, min(S - row0, p.Lc));
+  const int HB = 1 << p.hbits, hshift = 32 - p.hbits;
+  for (int i = tid; i < G * HB; i += kPT) hist[i] = 0u;
+  __syncthreads();
+  if (n > 0) {
+    const int R1 = p.r1;
+    const int nbox = ceil_div(n, R1);
+    const unsigned box_bytes = (unsigned)(R1 * p.dbox * E);
+    const int mine = nbox > w ? ceil_div(nbox - w, kPW) : 0;  // boxes w, w + kPW, ...
+    auto issue = [&](int k, const RingPos& at) {
+      mbar_expect_tx(&wbar[at.slot], box_bytes);
+      tma_box4d(wring + at.slot * SB, lead_map, 0, row0 + (w + k * kPW) * R1, hk, b, &wbar[at.slot]);
+    };
+    if (lane == 0) {
+      RingPos q = rp;
+      for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
+    }
+    const size_t qrow0 = (size_t)b * p.Hq + (size_t)hk * G;
+    const int nch1 = p.dbox / VEC;
+    const int LPR1 = next_pow2(nch1);
+    const int sl = lane % LPR1;
+    float q1[G_T][VEC];
+#pragma unroll
+    for (int g = 0; g < G_T; ++g)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const int col = sl * VEC + v;
+        q1[g][v] = (g < G && col < p.d && sl < nch1) ? p.q_hat[(qrow0 + g) * p.D + col] : 0.f;
+      }
+    uint32_t* keys_u = p.keys + (size_t)u * G * p.kstride + row0;
+    float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap + row0 : nullptr;
+    for (int k = 0; k < mine; ++k, rp.advance(1)) {
+      mbar_wait(&wbar[rp.slot], rp.phase);
+      const uint8_t* tile = wring + rp.slot * SB;
+      const int i = w + k * kPW;
+      const int rows_here = min(R1, n - i * R1);
+      uint32_t* k0 = keys_u + i * R1;
+      float* a0 = approx_u ? approx_u + i * R1 : nullptr;
+      switch (LPR1) {
+        case 1: lead_consume<T, G_T, VEC, 1>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
+        case 2: lead_consume<T, G_T, VEC, 2>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
+        case 4: lead_consume<T, G_T, VEC, 4>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
+        case 8: lead_consume<T, G_T, VEC, 8>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
+        case 16: lead_consume<T, G_T, VEC, 16>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
+        default: lead_consume<T, G_T, VEC, 32>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
+      }
+      __syncwarp();  // every lane is done with the slot before it is refilled
+      if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+    }
+  }
+  __syncthreads();
+  uint32_t* gh = p.hist + (size_t)u * G * HB;
+  for (int i = tid; i < G * HB; i += kPT) {
+    const uint32_t v = hist[i];
+    if (v) atomicAdd(&gh[i], v);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) sh.last = atomicAdd(&p.ctrl[2 + 4 * (size_t)u], 1u) == (unsigned)nparts - 1u;
+  __syncthreads();
+  if (sh.last) {
+    __threadfence();
+    if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();
+    select_unit<G_T>(p, u, S, ring, hist, sh);
+    return 3;
+  }
+  return 1;
+}
+
+// ------------------------------------------------------------------ item B
+template <int G_T>
+__device__ void merge_unit(const PipeParams& p, int u, int S, PipeShared& sh) {
+  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const int G = p.G, D = p.D, ldp = D + 2;
+  uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
+  const size_t qrow0 = ((size_t)(u / p.Hkv) * p.Hq) + (size_t)(u % p.Hkv) * G;
+  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
+  const float* part = p.part + (size_t)u * p.nA * G * ldp;
+  for (int i = tid; i < G * D; i += kPT) {
+    const int g = i / D, col = i % D;
+    float mm = -CUDART_INF_F, ll = 0.f, aa = 0.f;
+    for (int q = 0; q < nparts; ++q) {
+      const float* f = part + ((size_t)q * G + g) * ldp;
+      float s1, s2;
+      merge_state(mm, ll, __ldcg(&f[D]), __ldcg(&f[D + 1]), s1, s2);
+      aa = aa * s1 + __ldcg(&f[col]) * s2;
+    }
+    p.out[(qrow0 + g) * D + col] = ll > 0.f ? aa / ll : 0.f;
+    if (col == 0) {
+      sh.gm[g] = mm;
+      sh.gl[g] = ll;
+    }
+  }
+  __syncthreads();
+  if (p.weights_out != nullptr) {  // softmax weights of each head's selection, ascending rows
+    const unsigned lt = (1u << lane) - 1u;
+    for (int g = 0; g < G; ++g) {
+      const unsigned long long Tc = __ldcg(&p.tcs[(size_t)u * G + g]);
+      const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
+      const float M = sh.gm[g], invL = 1.f / sh.gl[g];
+      const float* lg = p.logits + ((size_t)u * G + g) * p.S_cap;
+      float* dst = p.weights_out + (qrow0 + g) * p.idx_stride;
+      unsigned emitted = 0;
+      for (int j0 = 0; j0 < S; j0 += kPT) {
+        const int j = j0 + tid;
+        const bool on = j < S && comp_key(__ldcg(&keys[j]), j) >= Tc;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) sh.wcnt[w][0] = __popc(bal);
+        __syncthreads();
+        unsigned before = 0, tot = 0;
+        for (int ww = 0; ww < kPW; ++ww) {
+          before += ww < w ? sh.wcnt[ww][0] : 0;
+          tot += sh.wcnt[ww][0];
+        }
+        if (on) dst[emitted + before + __popc(bal & lt)] = exp2f(__ldcg(&lg[j]) - M) * invL;
+        emitted += tot;
+        __syncthreads();
+      }
+    }
+  }
+  if (tid == 0) {
+    cu[1] = 0u;
+    cu[2] = 0u;
+  }
+}
+
+// B(u, q): rows [q * Lc, (q + 1) * Lc).  kNB 128-row blocks per warp.
+template <typename T, int G_T, int VEC, int D_T>
+__device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u, int q,
+                       uint8_t* ring, uint8_t* wring, uint64_t* wbar, uint32_t* ents, RingPos& rp, PipeShared& sh) {
+  constexpr int E = sizeof(T);
+  constexpr int LPR3 = D_T / VEC;  // lanes per V row
+  constexpr int RPW3 = 32 / LPR3;
+  constexpr int ROWB = D_T * E;
+  constexpr int kNB = G_T >= 4 ? 1 : 4 / G_T;  // Lc == kNB * 128 * kPW (host)
+  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const int nsw = p.nst, SB = p.stage_bytes;
+  const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G, D = D_T;
+  int S = p.lens[b];
+  S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
+  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
+  if (q >= nparts) return 0;  // past this unit's length: not an arrival
+  const int row0 = q * p.Lc;
+  const int nrows = max(0, min(S - row0, p.Lc));
+  uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
+  if (tid == 0) {
+    unsigned long long spins = 0;
+    while (ld_acquire(&cu[2]) == 0u) {
+      __nanosleep(64);
+      if (++spins > (1ull << 28)) {
+        printf("loki pipe: unit %d never became ready (block %d)\n", u, (int)blockIdx.x);
+        __trap();
+      }
+    }
+  }
+  __syncthreads();
+  const bool split = p.split_k != 0;
+  const size_t qrow0 = (size_t)b * p.Hq + (size_t)hk * G;
+  float* apx = reinterpret_cast<float*>(ents + p.Lc);  // [G][Lc] phase-1 partial logits, log2 domain
+  // this part's selected rows, ascending, with head masks: one L2 round trip for the keys
+  int n = 0;
+  if (nrows > 0) {
+    const uint32_t* kbase = p.keys + (size_t)u * G * p.kstride;
+    unsigned long long Tc[G_T];
+#pragma unroll
+    for (int g = 0; g < G_T; ++g) Tc[g] = g < G ? __ldcg(&p.tcs[(size_t)u * G + g]) : ~0ull;
+    const int wr0 = row0 + w * kNB * 128;  // this warp's rows [wr0, wr0 + kNB * 128)
+    const int rend = row0 + nrows;
+    uint4 kk[kNB][G_T];
+#pragma unroll
+    for (int bq = 0; bq < kNB; ++bq) {
+      const int jb = wr0 + bq * 128 + 4 * lane;
+#pragma unroll
+      for (int g = 0; g < G_T; ++g)
+        kk[bq][g] = (g < G && jb < rend) ? ld_keys4(kbase + (size_t)g * p.kstride, jb) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    unsigned m[kNB][4];
+    int ns = 0;
+#pragma unroll
+    for (int bq = 0; bq < kNB; ++bq)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = wr0 + bq * 128 + 4 * lane + e;
+        unsigned mm = 0;
+#pragma unroll
+        for (int g = 0; g < G_T; ++g)
+          if (g < G && j < rend && comp_key(u4_at(kk[bq][g], e), j) >= Tc[g]) mm |= 1u << g;
+        m[bq][e] = mm;
+        ns += mm != 0;
+      }
+    int wtot;
+    const int lpos = warp_excl_scan(ns, &wtot);
+    if (lane == 0) sh.wcnt[w][0] = wtot;
+    __syncthreads();
+    int pos = lpos;
+    for (int ww = 0; ww < kPW; ++ww) {
+      pos += ww < w ? sh.wcnt[ww][0] : 0;
+      n += sh.wcnt[ww][0];
+    }
+    // lane order inside a warp: block-major (bq), then lane, then e
+    int bpos[kNB];
+    {
+      int acc = 0;
+#pragma unroll
+      for (int bq = 0; bq < kNB; ++bq) {
+        int c = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c += m[bq][e] != 0;
+        int tot;
+        const int ex = warp_excl_scan(c, &tot);
+        bpos[bq] = pos - lpos + acc + ex;  // warp base + earlier blocks + earlier lanes
+        acc += tot;
+      }
+    }
+#pragma unroll
+    for (int bq = 0; bq < kNB; ++bq) {
+      int qd = bpos[bq];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (m[bq][e]) {
+          const int j = wr0 + bq * 128 + 4 * lane + e;
+          ents[qd] = (m[bq][e] << 24) | (uint32_t)j;
+          if (split)
+#pragma unroll
+            for (int g = 0; g < G_T; ++g)
+              if (g < G) apx[g * p.Lc + qd] = key_to_float(u4_at(kk[bq][g], e)) * p.qscale;
+          ++qd;
+        }
+      }
+    }
+    if (p.idx_out != nullptr) {  // per-head ascending indices at the part's published offset
+#pragma unroll
+      for (int g = 0; g < G_T; ++g) {
+        if (g >= G) break;
+        int cg = 0;
+#pragma unroll
+        for (int bq = 0; bq < kNB; ++bq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cg += (m[bq][e] >> g) & 1u;
+        const int gtot = __reduce_add_sync(0xffffffffu, cg);
+        if (lane == 0) sh.wcnt[w][1 + g] = gtot;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int g = 0; g < G_T; ++g) {
+        if (g >= G) break;
+        int base = (int)__ldcg(&p.poff[((size_t)u * G + g) * p.nA + q]);
+        for (int ww = 0; ww < w; ++ww) base += sh.wcnt[ww][1 + g];
+        int32_t* dst = p.idx_out + (qrow0 + g) * p.idx_stride;
+#pragma unroll
+        for (int bq = 0; bq < kNB; ++bq) {
+          int c = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) c += (m[bq][e] >> g) & 1u;
+          int tot;
+          int qd = base + warp_excl_scan(c, &tot);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if ((m[bq][e] >> g) & 1u) dst[qd++] = wr0 + bq * 128 + 4 * lane + e;
+          base += tot;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  const int kcol0 = split ? p.d : 0;  // first gathered K column
+  const int KW = D - kcol0;           // gathered K columns
+  const int KROWB = KW * E;
+  const int R3 = p.r3;
+  const int nstage = ceil_div(n, R3);
+  const unsigned stage_bytes = (unsigned)(R3 * (KROWB + ROWB));
+  const bool want_logits = p.weights_out != nullptr;
+  const int row_base = (int)(((long long)b * p.Hkv + hk) * p.unit_rows);
+  const int mine = nstage > w ? ceil_div(nstage - w, kPW) : 0;  // stages w, w + kPW, ...
+  auto issue = [&](int k, const RingPos& at) {
+    const int st = w + k * kPW;
+    uint8_t* dst = wring + at.slot * SB;
+    if (lane == 0) mbar_expect_tx(&wbar[at.slot], stage_bytes);
+    int row = -1;  // lane t < R3 resolves row t of the stage; -1 = out of bounds, zero-filled
+    const int t = st * R3 + lane;
+    if (lane < R3 && t < n) row = row_base + (int)(ents[t] & 0xFFFFFFu);
+    for (int qq = 0; qq < R3 / 4; ++qq) {
+      const int a0 = __shfl_sync(0xffffffffu, row, 4 * qq);
+      const int a1 = __shfl_sync(0xffffffffu, row, 4 * qq + 1);
+      const int a2 = __shfl_sync(0xffffffffu, row, 4 * qq + 2);
+      const int a3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
+      if (lane == 0) {
+        tma_gather4(dst + qq * 4 * KROWB, krow_map, kcol0, a0, a1, a2, a3, &wbar[at.slot]);
+        tma_gather4(dst + R3 * KROWB + qq * 4 * ROWB, vrow_map, 0, a0, a1, a2, a3, &wbar[at.slot]);
+      }
+    }
+  };
+  {
+    RingPos qp = rp;
+    for (int k = 0; k < nsw && k < mine; ++k, qp.advance(1)) issue(k, qp);
+  }
+  float acc[G_T][VEC];
+  float m[G_T], l[G_T];
+#pragma unroll
+  for (int g = 0; g < G_T; ++g) {
+    m[g] = -CUDART_INF_F;
+    l[g] = 0.f;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[g][v] = 0.f;
+  }
+  const int r = lane / LPR3, sl = lane % LPR3;
+  const bool k_on = sl * VEC < KW;
+  float q3[G_T][VEC];
+#pragma unroll
+  for (int g = 0; g < G_T; ++g)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const int col = kcol0 + sl * VEC + v;
+      q3[g][v] = (g < G && k_on && col < D) ? p.q_hat[(qrow0 + g) * D + col] * p.qscale : 0.f;
+    }
+  constexpr int U = 2;  // rows per lane slot whose logits are formed before the softmax updates
+  for (int k = 0; k < mine; ++k, rp.advance(1)) {
+    mbar_wait(&wbar[rp.slot], rp.phase);
+    const int st = w + k * kPW;
+    const uint8_t* kt = wring + rp.slot * SB;
+    const uint8_t* vt = kt + R3 * KROWB;
+    for (int ps = 0; ps < R3 / RPW3; ps += U) {  // host: (R3 / RPW3) % U == 0
+      float x[U][G_T];
+      int jr[U];
+      unsigned msk[U];
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int rr = (ps + uu) * RPW3 + r;
+        const int t = st * R3 + rr;
+        const bool ok = t < n;
+        const uint32_t e = ok ? ents[t] : 0u;
+        jr[uu] = (int)(e & 0xFFFFFFu);
+        msk[uu] = e >> 24;
+        float kx[VEC];
+        if (k_on) lds_chunk<T, VEC>(kt + rr * KROWB + sl * VEC * E, kx);
+        else
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) kx[v] = 0.f;
+#pragma unroll
+        for (int g = 0; g < G_T; ++g) {
+          float s = 0.f;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) s = fmaf(q3[g][v], kx[v], s);
+          s = sum_lanes<LPR3>(s);
+          if (split && ok && g < G) s += apx[g * p.Lc + t];
+          x[uu][g] = s;
+        }
+      }
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int rr = (ps + uu) * RPW3 + r;
+        float vx[VEC];
+        lds_chunk<T, VEC>(vt + rr * ROWB + sl * VEC * E, vx);
+#pragma unroll
+        for (int g = 0; g < G_T; ++g) {
+          if (msk[uu] & (1u << g)) {
+            const float xv = x[uu][g];
+            if (want_logits && sl == 0) p.logits[((size_t)u * G + g) * p.S_cap + jr[uu]] = xv;
+            const float mn = fmaxf(m[g], xv);
+            const float sc = exp2f(m[g] - mn);
+            const float pe = exp2f(xv - mn);
+            l[g] = l[g] * sc + pe;
+            m[g] = mn;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[g][v] = fmaf(pe, vx[v], acc[g][v] * sc);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (k + nsw < mine) issue(k + nsw, rp);
+  }
+
+  // merge lanes sharing columns, then warps in fixed order, into this part's state
+#pragma unroll
+  for (int g = 0; g < G_T; ++g) {
+    for (int off = LPR3; off < 32; off <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m[g], off);
+      const float l2 = __shfl_xor_sync(0xffffffffu, l[g], off);
+      float s1, s2;
+      merge_state(m[g], l[g], m2, l2, s1, s2);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const float a2 = __shfl_xor_sync(0xffffffffu, acc[g][v], off);
+        acc[g][v] = acc[g][v] * s1 + a2 * s2;
+      }
+    }
+  }
+  const int ldp = D + 2;
+  float* wpart = reinterpret_cast<float*>(ring);  // [kPW][G_T][D + 2]; every ring slot has been consumed
+  __syncthreads();
+  if (r == 0) {
+#pragma unroll
+    for (int g = 0; g < G_T; ++g) {
+      if (g >= G) break;
+      float* dstp = wpart + ((size_t)w * G_T + g) * ldp;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) dstp[sl * VEC + v] = acc[g][v];
+      if (sl == 0) {
+        dstp[D] = m[g];
+        dstp[D + 1] = l[g];
+      }
+    }
+  }
+  __syncthreads();
+  float* gpart = p.part + (((size_t)u * p.nA + q) * G) * ldp;
+  for (int i = tid; i < G * ldp; i += kPT) {
+    const int g = i / ldp, col = i % ldp;
+    float mm = -CUDART_INF_F, ll = 0.f, aa = 0.f;
+    for (int ww = 0; ww < kPW; ++ww) {
+      const float* src = wpart + ((size_t)ww * G_T + g) * ldp;
+      float s1, s2;
+      merge_state(mm, ll, src[D], src[D + 1], s1, s2);
+      if (col < D) aa = aa * s1 + src[col] * s2;
+    }
+    gpart[(size_t)g * ldp + col] = col < D ? aa : (col == D ? mm : ll);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) sh.last = atomicAdd(&cu[1], 1u) == (unsigned)nparts - 1u;
+  __syncthreads();
+  if (sh.last) {
+    __threadfence();
+    if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();
+    merge_unit<G_T>(p, u, S, sh);
+    return 4;
+  }
+  return 2;
+}
+
+// ------------------------------------------------------------------ kernel
+template <typename T, int G_T, int VEC, int D_T>
+__global__ void __launch_bounds__(kPT) pipe_decode_kernel(const PipeParams p,
+                                                          const __grid_constant__ CUtensorMap lead_map,
+                                                          const __grid_constant__ CUtensorMap krow_map,
+                                                          const __grid_constant__ CUtensorMap vrow_map) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ PipeShared sh;
+  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
+  const int nsw = p.nst;
+  uint8_t* ring = smem + p.off_ring;
+  uint8_t* wring = ring + (size_t)w * nsw * p.stage_bytes;
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bars) + (size_t)w * nsw;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + p.off_hist);
+  uint32_t* ents = reinterpret_cast<uint32_t*>(smem + p.off_ents);
+  if (lane == 0) {
+    for (int s = 0; s < nsw; ++s) mbar_init(&wbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid == 0) {
+    prefetch_desc(&lead_map);
+    prefetch_desc(&krow_map);
+    prefetch_desc(&vrow_map);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended rows are visible
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (tid == 0) sh.next_ticket = atomicAdd(&p.ctrl[0], 1u);
+  __syncthreads();
+  RingPos rp(nsw);
+  const int per_slot = 2 * p.nA;  // A(u, 0..nA-1) then B(u - lag, 0..nA-1)
+  for (;;) {
+    const unsigned t = sh.next_ticket;
+    __syncthreads();
+    if ((long long)t >= p.n_tickets) {
+      if (tid == 0 && atomicAdd(&p.ctrl[1], 1u) == gridDim.x - 1u) {  // last CTA out resets the counters
+        atomicExch(&p.ctrl[0], 0u);
+        atomicExch(&p.ctrl[1], 0u);
+      }
+      break;
+    }
+    if (tid == 0) sh.next_ticket = atomicAdd(&p.ctrl[0], 1u);  // prefetched; read after the item's barriers
+    const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
+    const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
+    int kind = 0;
+    if (r < p.nA) {
+      if (slot < p.units) kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, rp, sh);
+    } else {
+      const int u = slot - p.lag;
+      if (u >= 0 && u < p.units)
+        kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, u, r - p.nA, ring, wring, wbar, ents, rp, sh);
+    }
+    fence_proxy_async();  // this item's generic shared-memory writes precede the next item's TMA writes
+    __syncthreads();
+    if (p.trace != nullptr && tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      long long* tr = p.trace + (size_t)t * 4;
+      tr[0] = t0;
+      tr[1] = globaltimer();
+      tr[2] = (long long)smid | ((long long)kind << 16) | ((long long)blockIdx.x << 32);
+      tr[3] = (kind >= 3) ? sh.t_sel : 0;
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+
+int pipe_warps() { return kPW; }
+
+size_t pipe_layout(int G_T, PipeParams* p) {
+  size_t off = 0;
+  p->off_ring = 0;
+  off += (size_t)kPW * p->nst * p->stage_bytes;
+  p->off_bars = (int)off;
+  off = align_up(off + (size_t)kPW * p->nst * 8, 16);
+  p->off_hist = (int)off;
+  const int hb = p->hbits > 8 ? p->hbits : 8;
+  off = align_up(off + (size_t)G_T * (1u << hb) * 4, 16);
+  p->off_ents = (int)off;
+  off = align_up(off + (size_t)p->Lc * 4 * (1 + (p->split_k ? G_T : 0)), 128);
+  p->cand_cap = (int)((size_t)kPW * p->nst * p->stage_bytes / 24);  // three u64 candidate buffers
+  return off;
+}
+
+template <typename T, int G_T, int VEC, int D_T>
+static cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st) {
+  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T>;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kPT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps);
+  return cudaLaunchKernelEx(&cfg, kern, p, m[0], m[1], m[2]);
+}
+
+template <typename T, int G_T, int VEC, int D_T>
+static int occupancy_t(size_t smem) {
+  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kPT, smem) != cudaSuccess) return 0;
+  return n;
+}
+
+// dispatch over (dtype, D, G_T); F is a functor template taking <T, G_T, VEC, D_T>
+#define LOKI_PIPE_DISPATCH(DTYPE, D, GT, CALL)                                                     \
+  do {                                                                                             \
+    if ((DTYPE) == LOKI_DTYPE_BF16) {                                                              \
+      switch ((D) * 16 + (GT)) {                                                                   \
+        case 64 * 16 + 1: return CALL(__nv_bfloat16, 1, 8, 64);                                    \
+        case 64 * 16 + 2: return CALL(__nv_bfloat16, 2, 8, 64);                                    \
+        case 64 * 16 + 4: return CALL(__nv_bfloat16, 4, 8, 64);                                    \
+        case 64 * 16 + 8: return CALL(__nv_bfloat16, 8, 4, 64);                                    \
+        case 128 * 16 + 1: return CALL(__nv_bfloat16, 1, 8, 128);                                  \
+        case 128 * 16 + 2: return CALL(__nv_bfloat16, 2, 8, 128);                                  \
+        case 128 * 16 + 4: return CALL(__nv_bfloat16, 4, 8, 128);                                  \
+        case 128 * 16 + 8: return CALL(__nv_bfloat16, 8, 4, 128);                                  \
+        case 256 * 16 + 1: return CALL(__nv_bfloat16, 1, 8, 256);                                  \
+        case 256 * 16 + 2: return CALL(__nv_bfloat16, 2, 8, 256);                                  \
+        case 256 * 16 + 4: return CALL(__nv_bfloat16, 4, 8, 256);                                  \
+        default: break;                                                                            \
+      }                                                                                            \
+    } else {                                                                                       \
+      switch ((D) * 16 + (GT)) {                                                                   \
+        case 64 * 16 + 1: return CALL(float, 1, 4, 64);                                            \
+        case 64 * 16 + 2: return CALL(float, 2, 4, 64);                                            \
+        case 64 * 16 + 4: return CALL(float, 4, 4, 64);                                            \
+        case 64 * 16 + 8: return CALL(float, 8, 4, 64);                                            \
+        case 128 * 16 + 1: return CALL(float, 1, 4, 128);                                          \
+        case 128 * 16 + 2: return CALL(float, 2, 4, 128);                                          \
+        case 128 * 16 + 4: return CALL(float, 4, 4, 128);                                          \
+        case 128 * 16 + 8: return CALL(float, 8, 4, 128);                                          \
+        default: break;                                                                            \
+      }                                                                                            \
+    }                                                                                              \
+  } while (0)
+
+bool pipe_supported(int dtype, int D, int G_T) {
+  if (dtype == LOKI_DTYPE_BF16) return (D == 64 || D == 128 || (D == 256 && G_T <= 4)) && G_T <= 8;
+  return (D == 64 || D == 128) && G_T <= 8;
+}
+
+int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem) {
+#define LOKI_OCC(T, GT, VEC, DT) occupancy_t<T, GT, VEC, DT>(smem)
+  LOKI_PIPE_DISPATCH(dtype, D, G_T, LOKI_OCC);
+#undef LOKI_OCC
+  return 0;
+}
+
+cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
+                        cudaStream_t st) {
+#define LOKI_LAUNCH(T, GT, VEC, DT) launch_pipe_t<T, GT, VEC, DT>(p, grid, smem, maps, st)
+  LOKI_PIPE_DISPATCH(dtype, p.D, G_T, LOKI_LAUNCH);
+#undef LOKI_LAUNCH
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace loki

@@ -59,7 +59,47 @@ torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1000 / a.reps
 print(f"{a.mode}: {us:.1f} us/launch, {nbytes / us / 1e3:.1f} GB/s algorithmic")
 
-if os.environ.get("LOKI_TRACE"):
+if os.environ.get("LOKI_TRACE") and call.plan()["ctas_per_unit"] == 0:
+    # persistent pipe kernel: per-ticket {start, end, smid | kind << 16 | block << 32}
+    import numpy as np
+
+    nbuf = 1 << 22
+    buf = torch.zeros(nbuf, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.loki_set_phase_trace(buf.data_ptr(), nbuf // 8))
+    call.run()
+    torch.cuda.synchronize()
+    _lib.check(lib.loki_set_phase_trace(None, 0))
+    t = buf.view(-1, 4).cpu().numpy()
+    t = t[t[:, 0] != 0]
+    kind = (t[:, 2] >> 16) & 0xFFFF
+    t0 = t[:, 0].min()
+    st, en = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
+    dur = en - st
+    print(f"pipe: {len(t)} tickets, span {en.max():.1f} us, blocks {len(np.unique(t[:, 2] >> 32))}")
+    for kd, nm in ((1, "A"), (3, "A+select"), (2, "B"), (4, "B+merge"), (0, "noop")):
+        m = kind == kd
+        if m.any():
+            print(f"  {nm:9s} n={m.sum():5d} median {np.median(dur[m]):7.2f} us  mean {dur[m].mean():7.2f}  max {dur[m].max():7.2f}  busy-share {dur[m].sum() / dur.sum() * 100:5.1f}%")
+    lastm = t[:, 3] != 0
+    tail = (t[lastm, 1] - t[lastm, 3]) / 1e3
+    for kd, nm in ((3, "select"), (4, "merge")):
+        m = kind[lastm] == kd
+        if m.any():
+            print(f"  {nm:9s} part: median {np.median(tail[m]):7.2f} us  mean {tail[m].mean():7.2f}  max {tail[m].max():7.2f}")
+    ab = np.array([1 if k in (1, 3) else 0 for k in kind])
+    bb_ = np.array([1 if k in (2, 4) else 0 for k in kind])
+    grid = np.linspace(0, en.max(), 40)
+    occA = [((st <= x) & (en > x) & (ab == 1)).sum() for x in grid]
+    occB = [((st <= x) & (en > x) & (bb_ == 1)).sum() for x in grid]
+    print("  CTAs in A / B over time:", " ".join(f"{a}/{b}" for a, b in zip(occA, occB)))
+    blk = t[:, 2] >> 32
+    idle = []
+    for bb in np.unique(blk):
+        mm = blk == bb
+        idle.append(en[mm].max() - dur[mm].sum())
+    print(f"  per-CTA idle (span - busy): median {np.median(idle):.1f} us; last CTA end - first CTA end {en.max() - np.min([en[blk == bb].max() for bb in np.unique(blk)]):.1f} us")
+elif os.environ.get("LOKI_TRACE"):
     import numpy as np
 
     plan = call.plan()
