@@ -264,9 +264,12 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   const int units = g.B * g.Hkv;
   const int e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   pl->G_T = G_T;
-  const int stage = env_int("LOKI_PIPE_STAGE_KB", 4) * 1024;
+  // tensor-core phase 3 (bf16): 16-row stages of K and V (64 * D bytes)
+  const bool mma = g.dtype == LOKI_DTYPE_BF16 && env_int("LOKI_PIPE_MMA", 1) != 0;
+  const int stage = mma ? 32 * g.D : env_int("LOKI_PIPE_STAGE_KB", 4) * 1024;
   if (!tma_geom(a, G_T, &pl->tg, stage)) return fail(LOKI_ERR_UNSUPPORTED, "pipe: TMA geometry");
   loki::PipeParams& p = pl->p;
+  p.mma = mma ? 1 : 0;
   p.nst = env_int("LOKI_PIPE_STAGES", 2);
   p.stage_bytes = stage;
   p.r1 = pl->tg.r1;
@@ -275,7 +278,12 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   p.hbits = G_T <= 2 ? 11 : (G_T == 4 ? 10 : 9);
   const int d = a->d < 1 ? 1 : a->d;
   const int vec = pl->tg.vec;
-  p.split_k = env_int("LOKI_SPLITK", 1) != 0 && d < g.D && d % vec == 0 && ((g.D - d) * e) % 32 == 0;
+  p.split_k = !mma && env_int("LOKI_SPLITK", 1) != 0 && d < g.D && d % vec == 0 && ((g.D - d) * e) % 32 == 0;
+  if (mma) p.r3 = 8;
+  // one lane per lead row when the row is a TMA swizzle span (64 / 128 B) and r1 covers whole lanes
+  const int lead_rb = p.dbox * e;
+  p.lead_swz = (G_T == 1 && (lead_rb == 64 || lead_rb == 128) && p.r1 % 64 == 0 && env_int("LOKI_LEAD_LPR", 1) != 0)
+                   ? lead_rb : 0;
   // chunk = part: kNB 128-row blocks per warp in the B-item row scan (loki_pipe.cu)
   const int kNB = G_T >= 4 ? 1 : 4 / G_T;
   const int Lc = kNB * 128 * loki::pipe_warps();
@@ -351,7 +359,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   p.trace = (loki::g_phase_trace != nullptr && p.n_tickets * 4 <= (long long)loki::g_phase_trace_ctas * 8)
                 ? loki::g_phase_trace : nullptr;
   loki::TmaDesc maps[3];
-  if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, maps))
+  if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, p.mma != 0, p.lead_swz, maps))
     return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
   cudaError_t e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream));
   if (e == cudaSuccess) e = cudaGetLastError();

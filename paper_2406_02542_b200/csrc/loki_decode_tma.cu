@@ -341,7 +341,7 @@ EncodeTiledFn encode_fn() {
 }
 
 bool encode4d(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_kv_geom& g, int box0, int box1,
-              CUtensorMapL2promotion promo) {
+              CUtensorMapL2promotion promo, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   const CUtensorMapDataType dt =
       g.dtype == LOKI_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -353,11 +353,12 @@ bool encode4d(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_kv_g
   cuuint32_t box[4] = {(cuuint32_t)box0, (cuuint32_t)box1, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(reinterpret_cast<CUtensorMap*>(out->bytes), dt, 4, const_cast<void*>(base), dims, str, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool encode_rows(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_kv_geom& g, int width = 0) {
+bool encode_rows(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_kv_geom& g, int width = 0,
+                 bool swizzle128 = false) {
   const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   const CUtensorMapDataType dt =
       g.dtype == LOKI_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -366,7 +367,8 @@ bool encode_rows(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_k
   cuuint32_t box[2] = {(cuuint32_t)(width > 0 ? width : g.D), 1};
   cuuint32_t es[2] = {1, 1};
   return enc(reinterpret_cast<CUtensorMap*>(out->bytes), dt, 2, const_cast<void*>(base), dims, str, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -384,11 +386,15 @@ bool encode_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, i
 }
 
 bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, int r1, int kcol0,
-                     TmaDesc* maps) {
+                     bool mma, int lead_swz, TmaDesc* maps) {
   EncodeTiledFn enc = encode_fn();
   if (enc == nullptr) return false;
-  return encode4d(enc, &maps[0], K, g, dbox, r1, CU_TENSOR_MAP_L2_PROMOTION_L2_64B) &&
-         encode_rows(enc, &maps[1], K, g, g.D - kcol0) && encode_rows(enc, &maps[2], V, g);
+  const CUtensorMapSwizzle ls = lead_swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                               : (lead_swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!encode4d(enc, &maps[0], K, g, dbox, r1, CU_TENSOR_MAP_L2_PROMOTION_L2_64B, ls)) return false;
+  if (mma)  // tensor-core phase 3: 128 B row halves, 128B-swizzled (conflict-free ldmatrix)
+    return encode_rows(enc, &maps[1], K, g, 64, true) && encode_rows(enc, &maps[2], V, g, 64, true);
+  return encode_rows(enc, &maps[1], K, g, g.D - kcol0) && encode_rows(enc, &maps[2], V, g);
 }
 
 template <typename T, int G_T, int VEC, int D_T>

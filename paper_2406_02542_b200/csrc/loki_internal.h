@@ -72,6 +72,8 @@ struct PipeParams {
   int units, Lc, nA, lag, hbits, cand_cap;
   long long n_tickets;
   int split_k;       // 1: phase 3 gathers K columns [d, D) only and reuses the phase-1 partial score
+  int mma;           // 1: tensor-core phase 3 (bf16 caches): 8-row stages of 128B-swizzled row halves
+  int lead_swz;      // 64 / 128: lead rows of that many bytes, TMA-swizzled, one lane per row (G == 1); 0: off
   uint32_t* ctrl;    // [2 + 4 * units]: ticket, exits, then per unit {A arrivals, B arrivals, ready, -}
   uint32_t* hist;    // [units][G][1 << hbits]
   uint32_t* keys;    // [units][G][kstride] order keys of the approx scores
@@ -141,7 +143,8 @@ cudaError_t launch_index_status(const int64_t* idx, int n, int64_t bound, int32_
 size_t pipe_layout(int G_T, PipeParams* p);
 bool pipe_supported(int dtype, int D, int G_T);
 // lead boxes {dbox, r1} (64 B promotion), K row gathers of columns [kcol0, D), V row gathers
-bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, int r1, int kcol0, TmaDesc* maps);
+bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, int r1, int kcol0, bool mma,
+                     int lead_swz, TmaDesc* maps);
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
                         cudaStream_t st);
 int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem);

@@ -79,6 +79,37 @@ __device__ __forceinline__ unsigned long long comp_key(uint32_t key, int j) {
   return ((unsigned long long)key << 32) | (unsigned long long)(~(uint32_t)j);
 }
 
+// ---- tensor-core helpers (phase 3 on bf16 caches)
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+// d += a (16x16 bf16, row) * b (16x8 bf16, col), fp32 accumulate
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// {lo -> bits 0..15, hi -> bits 16..31}, round to nearest even
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// x = hi + lo with hi, lo bf16 (relative error of hi + lo ~ 2^-17)
+__device__ __forceinline__ float bf16_hi(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float bf16_lo(float x) { return x - bf16_hi(x); }
+// 16 B chunk c of row r inside a 128B-swizzled block of 128 B rows (TMA SWIZZLE_128B)
+__device__ __forceinline__ uint32_t swz128(uint32_t base, int r, int c) {
+  return base + (uint32_t)(r * 128) + (uint32_t)(((c ^ (r & 7)) << 4));
+}
+
 __device__ __forceinline__ int k_of(const PipeParams& p, int S) {
   if (S <= 0) return 0;
   return p.k_fixed > 0 ? (p.k_fixed < S ? p.k_fixed : S) : resolve_fraction(p.k_f, S);
@@ -309,8 +340,8 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem
       if (cnt == need) {
         Tc = nb >= 64 ? P : (P << (64 - nb));
       } else {  // <= 256 distinct candidates: the need-th largest by direct rank
-        if (tid < ncand) {
-          const unsigned long long c = src[tid];
+        for (int ci = tid; ci < ncand; ci += kPT) {
+          const unsigned long long c = src[ci];
           unsigned rank = 0;
           for (int i = 0; i < ncand; ++i) rank += src[i] > c;
           if (rank == need - 1) sh.tsel = c;
@@ -414,6 +445,62 @@ __device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t*
   }
 }
 
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long pk2(uint32_t lo, uint32_t hi) {
+  return ((unsigned long long)hi << 32) | lo;
+}
+
+// Phase-1 stage consumed by ONE warp with one lane per row (single query
+// head): RB-byte lead rows, TMA-swizzled (64 B: chunk ^ (row >> 1 & 3); 128 B:
+// chunk ^ (row & 7)) so the 16 B row reads are conflict-free; packed fp32 FMA
+// (two partial sums, any order is inside the fp32 tie band); the key and
+// approx stores are coalesced.
+template <typename T, int RB>
+__device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint8_t* tile, int rows_here,
+                                                 const unsigned long long (&q2)[32], uint32_t* keys0,
+                                                 float* approx0, uint32_t* hist, int hshift) {
+  constexpr int NCH = RB / 16;
+  const int lane = lane_id();
+  for (int r0 = 0; r0 < p.r1; r0 += 64) {
+    uint4 v[2][NCH];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int rr = r0 + 32 * i + lane;
+      const int sw = RB == 64 ? ((rr >> 1) & 3) : (rr & 7);
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+        v[i][c] = *reinterpret_cast<const uint4*>(tile + rr * RB + ((c ^ sw) << 4));
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      unsigned long long acc = 0ull;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint32_t wv[4] = {v[i][c].x, v[i][c].y, v[i][c].z, v[i][c].w};
+        if constexpr (sizeof(T) == 2) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc = ffma2(pk2(wv[e] << 16, wv[e] & 0xFFFF0000u), q2[c * 4 + e], acc);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) acc = ffma2(pk2(wv[2 * e], wv[2 * e + 1]), q2[c * 2 + e], acc);
+        }
+      }
+      const float sc = __uint_as_float((uint32_t)acc) + __uint_as_float((uint32_t)(acc >> 32));
+      const int rr = r0 + 32 * i + lane;
+      if (rr < rows_here) {
+        const uint32_t key = order_key(sc);
+        keys0[rr] = key;
+        if (approx0 != nullptr) approx0[rr] = sc;
+        atomicAdd(&hist[key >> hshift], 1u);
+      }
+    }
+  }
+}
+
 template <typename T, int G_T, int VEC>
 __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, int c, uint8_t* ring,
                        uint8_t* wring, uint64_t* wbar, uint32_t* hist, RingPos& rp, PipeShared& sh) {
@@ -457,6 +544,32 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
       }
     uint32_t* keys_u = p.keys + (size_t)u * G * p.kstride + row0;
     float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap + row0 : nullptr;
+    constexpr int E = sizeof(T);
+    if (G_T == 1 && p.lead_swz != 0) {  // one lane per row (swizzled lead rows)
+      constexpr int Q2 = 32;  // element pairs of the widest lead row (128 B of bf16)
+      unsigned long long q2[Q2];
+#pragma unroll
+      for (int j = 0; j < Q2; ++j) {
+        const int c0 = 2 * j, c1 = 2 * j + 1;
+        const float a = c0 < p.d ? p.q_hat[qrow0 * p.D + c0] : 0.f;
+        const float bq = c1 < p.d ? p.q_hat[qrow0 * p.D + c1] : 0.f;
+        q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
+      }
+      for (int k = 0; k < mine; ++k, rp.advance(1)) {
+        mbar_wait(&wbar[rp.slot], rp.phase);
+        const uint8_t* tile = wring + rp.slot * SB;
+        const int i = w + k * kPW;
+        const int rows_here = min(R1, n - i * R1);
+        uint32_t* k0 = keys_u + i * R1;
+        float* a0 = approx_u ? approx_u + i * R1 : nullptr;
+        if (p.lead_swz == 64)
+          lead_consume_lpr<T, 64>(p, tile, rows_here, q2, k0, a0, hist, hshift);
+        else
+          lead_consume_lpr<T, 128>(p, tile, rows_here, q2, k0, a0, hist, hshift);
+        __syncwarp();
+        if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+      }
+    } else
     for (int k = 0; k < mine; ++k, rp.advance(1)) {
       mbar_wait(&wbar[rp.slot], rp.phase);
       const uint8_t* tile = wring + rp.slot * SB;
@@ -549,6 +662,355 @@ __device__ void merge_unit(const PipeParams& p, int u, int S, PipeShared& sh) {
   if (tid == 0) {
     cu[1] = 0u;
     cu[2] = 0u;
+  }
+}
+
+template <typename T, int G_T, int VEC, int D_T>
+__device__ void stream_B_simt(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u,
+                              int n, int row_base, size_t qrow0, const uint32_t* ents, const float* apx, uint8_t* wring,
+                              uint64_t* wbar, RingPos& rp, float* wpart) {
+  constexpr int E = sizeof(T);
+  constexpr int LPR3 = D_T / VEC;  // lanes per V row
+  constexpr int RPW3 = 32 / LPR3;
+  constexpr int ROWB = D_T * E;
+  const int lane = lane_id(), w = warp_id();
+  const int nsw = p.nst, SB = p.stage_bytes;
+  const int G = p.G, D = D_T;
+  const bool split = p.split_k != 0;
+  const int kcol0 = split ? p.d : 0;  // first gathered K column
+  const int KW = D - kcol0;           // gathered K columns
+  const int KROWB = KW * E;
+  const int R3 = p.r3;
+  const int nstage = ceil_div(n, R3);
+  const unsigned stage_bytes = (unsigned)(R3 * (KROWB + ROWB));
+  const bool want_logits = p.weights_out != nullptr;
+  const int mine = nstage > w ? ceil_div(nstage - w, kPW) : 0;  // stages w, w + kPW, ...
+  auto issue = [&](int k, const RingPos& at) {
+    const int st = w + k * kPW;
+    uint8_t* dst = wring + at.slot * SB;
+    if (lane == 0) mbar_expect_tx(&wbar[at.slot], stage_bytes);
+    int row = -1;  // lane t < R3 resolves row t of the stage; -1 = out of bounds, zero-filled
+    const int t = st * R3 + lane;
+    if (lane < R3 && t < n) row = row_base + (int)(ents[t] & 0xFFFFFFu);
+    for (int qq = 0; qq < R3 / 4; ++qq) {
+      const int a0 = __shfl_sync(0xffffffffu, row, 4 * qq);
+      const int a1 = __shfl_sync(0xffffffffu, row, 4 * qq + 1);
+      const int a2 = __shfl_sync(0xffffffffu, row, 4 * qq + 2);
+      const int a3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
+      if (lane == 0) {
+        tma_gather4(dst + qq * 4 * KROWB, krow_map, kcol0, a0, a1, a2, a3, &wbar[at.slot]);
+        tma_gather4(dst + R3 * KROWB + qq * 4 * ROWB, vrow_map, 0, a0, a1, a2, a3, &wbar[at.slot]);
+      }
+    }
+  };
+  {
+    RingPos qp = rp;
+    for (int k = 0; k < nsw && k < mine; ++k, qp.advance(1)) issue(k, qp);
+  }
+  float acc[G_T][VEC];
+  float m[G_T], l[G_T];
+#pragma unroll
+  for (int g = 0; g < G_T; ++g) {
+    m[g] = -CUDART_INF_F;
+    l[g] = 0.f;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[g][v] = 0.f;
+  }
+  const int r = lane / LPR3, sl = lane % LPR3;
+  const bool k_on = sl * VEC < KW;
+  float q3[G_T][VEC];
+#pragma unroll
+  for (int g = 0; g < G_T; ++g)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const int col = kcol0 + sl * VEC + v;
+      q3[g][v] = (g < G && k_on && col < D) ? p.q_hat[(qrow0 + g) * D + col] * p.qscale : 0.f;
+    }
+  constexpr int U = 2;  // rows per lane slot whose logits are formed before the softmax updates
+  for (int k = 0; k < mine; ++k, rp.advance(1)) {
+    mbar_wait(&wbar[rp.slot], rp.phase);
+    const int st = w + k * kPW;
+    const uint8_t* kt = wring + rp.slot * SB;
+    const uint8_t* vt = kt + R3 * KROWB;
+    for (int ps = 0; ps < R3 / RPW3; ps += U) {  // host: (R3 / RPW3) % U == 0
+      float x[U][G_T];
+      int jr[U];
+      unsigned msk[U];
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int rr = (ps + uu) * RPW3 + r;
+        const int t = st * R3 + rr;
+        const bool ok = t < n;
+        const uint32_t e = ok ? ents[t] : 0u;
+        jr[uu] = (int)(e & 0xFFFFFFu);
+        msk[uu] = e >> 24;
+        float kx[VEC];
+        if (k_on) lds_chunk<T, VEC>(kt + rr * KROWB + sl * VEC * E, kx);
+        else
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) kx[v] = 0.f;
+#pragma unroll
+        for (int g = 0; g < G_T; ++g) {
+          float s = 0.f;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) s = fmaf(q3[g][v], kx[v], s);
+          s = sum_lanes<LPR3>(s);
+          if (split && ok && g < G) s += apx[g * p.Lc + t];
+          x[uu][g] = s;
+        }
+      }
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu) {
+        const int rr = (ps + uu) * RPW3 + r;
+        float vx[VEC];
+        lds_chunk<T, VEC>(vt + rr * ROWB + sl * VEC * E, vx);
+#pragma unroll
+        for (int g = 0; g < G_T; ++g) {
+          if (msk[uu] & (1u << g)) {
+            const float xv = x[uu][g];
+            if (want_logits && sl == 0) p.logits[((size_t)u * G + g) * p.S_cap + jr[uu]] = xv;
+            const float mn = fmaxf(m[g], xv);
+            const float sc = exp2f(m[g] - mn);
+            const float pe = exp2f(xv - mn);
+            l[g] = l[g] * sc + pe;
+            m[g] = mn;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[g][v] = fmaf(pe, vx[v], acc[g][v] * sc);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (k + nsw < mine) issue(k + nsw, rp);
+  }
+
+  // merge lanes sharing columns, then warps in fixed order, into this part's state
+#pragma unroll
+  for (int g = 0; g < G_T; ++g) {
+    for (int off = LPR3; off < 32; off <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m[g], off);
+      const float l2 = __shfl_xor_sync(0xffffffffu, l[g], off);
+      float s1, s2;
+      merge_state(m[g], l[g], m2, l2, s1, s2);
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const float a2 = __shfl_xor_sync(0xffffffffu, acc[g][v], off);
+        acc[g][v] = acc[g][v] * s1 + a2 * s2;
+      }
+    }
+  }
+  const int ldp = D + 2;
+  __syncthreads();
+  if (r == 0) {
+#pragma unroll
+    for (int g = 0; g < G_T; ++g) {
+      if (g >= G) break;
+      float* dstp = wpart + ((size_t)w * G_T + g) * ldp;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) dstp[sl * VEC + v] = acc[g][v];
+      if (sl == 0) {
+        dstp[D] = m[g];
+        dstp[D + 1] = l[g];
+      }
+    }
+  }
+}
+
+// Phase 3 on the tensor cores (bf16 caches).  A stage is 8 gathered rows
+// (4 KB at D = 128: many small stages keep 16 warps per SM issuing gathers,
+// tools/gatherbench.cu): K and V as 128 B row halves, 128B-swizzled by TMA so
+// ldmatrix is conflict-free.  Per stage, with the 8 rows as M rows 0..7 of
+// m16n8k16 (rows 8..15 zero):  S^T[8 x 8] = K[8 x D] . Qc[D x 8]  and
+// O^T[D x 8] += V^T[D x 8] . P^T[8 x 8]  (fp32 accumulate).  Columns carry
+// (head, hi / lo part): q * qscale and the softmax weights are split into two
+// bf16 terms, so both products keep ~2^-17 relative accuracy.
+// G <= 4: column 2h + part;  G == 8: columns = heads, hi and lo in two mmas.
+template <int G_T, int D_T>
+__device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u,
+                             int n, int row_base, size_t qrow0, const uint32_t* ents, uint8_t* wring, uint64_t* wbar,
+                             RingPos& rp, float* wpart) {
+  constexpr int NH = D_T / 64;             // 128 B row halves
+  constexpr int KS = D_T / 16;             // k-steps of q.K == m-tiles of P.V
+  constexpr int R = 8;                     // rows per stage
+  constexpr int HW = R * 128;              // bytes of one half block (one swizzle atom)
+  constexpr int NHL = G_T == 8 ? 2 : 1;    // heads per lane
+  constexpr bool kSplitCols = G_T < 8;
+  const int lane = lane_id(), w = warp_id();
+  const int G = p.G;
+  const int nsw = p.nst, SB = p.stage_bytes;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int nstage = ceil_div(n, R);
+  const unsigned stage_bytes = (unsigned)(R * D_T * 2 * 2);
+  const bool want_logits = p.weights_out != nullptr;
+  const int mine = nstage > w ? ceil_div(nstage - w, kPW) : 0;  // stages w, w + kPW, ...
+  auto issue = [&](int k, const RingPos& at) {
+    const int st = w + k * kPW;
+    uint8_t* dst = wring + at.slot * SB;
+    if (lane == 0) mbar_expect_tx(&wbar[at.slot], stage_bytes);
+    int row = -1;  // -1: out of bounds, zero-filled
+    const int t = st * R + lane;
+    if (lane < R && t < n) row = row_base + (int)(ents[t] & 0xFFFFFFu);
+#pragma unroll
+    for (int qq = 0; qq < R / 4; ++qq) {
+      const int a0 = __shfl_sync(0xffffffffu, row, 4 * qq);
+      const int a1 = __shfl_sync(0xffffffffu, row, 4 * qq + 1);
+      const int a2 = __shfl_sync(0xffffffffu, row, 4 * qq + 2);
+      const int a3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
+      if (lane == 0) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          tma_gather4(dst + h * HW + qq * 512, krow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
+          tma_gather4(dst + (NH + h) * HW + qq * 512, vrow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
+        }
+      }
+    }
+  };
+  {
+    RingPos qp = rp;
+    for (int k = 0; k < nsw && k < mine; ++k, qp.advance(1)) issue(k, qp);
+  }
+  // B operand of S^T = K . Qc: lane holds Qc[16 ks + 2 t4 + {0, 1, 8, 9}][g8]
+  uint32_t qb[KS][2], ql[G_T == 8 ? KS : 1][2];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k0 = 16 * ks + 2 * t4;
+    const int head = kSplitCols ? (g8 >> 1) : g8;
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int dim = k0 + (i & 1) + (i >> 1) * 8;
+      v[i] = head < G ? p.q_hat[(qrow0 + head) * D_T + dim] * p.qscale : 0.f;
+    }
+    if (kSplitCols) {
+      const bool lo = g8 & 1;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = lo ? bf16_lo(v[i]) : v[i];
+      qb[ks][0] = pack_bf16(v[0], v[1]);
+      qb[ks][1] = pack_bf16(v[2], v[3]);
+    } else {
+      qb[ks][0] = pack_bf16(v[0], v[1]);
+      qb[ks][1] = pack_bf16(v[2], v[3]);
+      ql[ks][0] = pack_bf16(bf16_lo(v[0]), bf16_lo(v[1]));
+      ql[ks][1] = pack_bf16(bf16_lo(v[2]), bf16_lo(v[3]));
+    }
+  }
+  float O[KS][4];
+#pragma unroll
+  for (int mt = 0; mt < KS; ++mt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) O[mt][i] = 0.f;
+  float m[NHL], l[NHL];
+#pragma unroll
+  for (int j = 0; j < NHL; ++j) {
+    m[j] = -CUDART_INF_F;
+    l[j] = 0.f;
+  }
+  const int rX = lane & 7;            // ldmatrix.x2 row (lanes 0..15 address two 8x8 matrices)
+  const int cX = (lane >> 3) & 1;     // second matrix: +8 columns (K) / +8 dims (V)
+  for (int k = 0; k < mine; ++k, rp.advance(1)) {
+    mbar_wait(&wbar[rp.slot], rp.phase);
+    const int st = w + k * kPW;
+    const uint32_t sb = smem_u32(wring + rp.slot * SB);
+    float S[4] = {0.f, 0.f, 0.f, 0.f}, S2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t a2[2];
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
+                   : "=r"(a2[0]), "=r"(a2[1])
+                   : "r"(swz128(sb + (ks >> 2) * HW, rX, ((ks & 3) << 1) | cX)));
+      const uint32_t a[4] = {a2[0], 0u, a2[1], 0u};
+      mma_bf16(S, a, qb[ks][0], qb[ks][1]);
+      if (!kSplitCols) mma_bf16(S2, a, ql[ks][0], ql[ks][1]);
+    }
+    const int tA = st * R + g8;
+    const uint32_t eA = tA < n ? ents[tA] : 0u;
+    float x[NHL], pr[NHL], sc[NHL];
+#pragma unroll
+    for (int j = 0; j < NHL; ++j) {
+      const int head = kSplitCols ? t4 : 2 * t4 + j;
+      x[j] = kSplitCols ? S[0] + S[1] : S[j] + S2[j];
+      const bool ok = head < G && ((eA >> (24 + head)) & 1u);
+      float tm = ok ? x[j] : -CUDART_INF_F;
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
+      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+      const float mn = fmaxf(m[j], tm);
+      sc[j] = (mn == -CUDART_INF_F) ? 1.f : exp2f(m[j] - mn);
+      pr[j] = ok ? exp2f(x[j] - mn) : 0.f;
+      l[j] = l[j] * sc[j] + pr[j];
+      m[j] = mn;
+      if (want_logits && ok) p.logits[((size_t)u * G + head) * p.S_cap + (eA & 0xFFFFFFu)] = x[j];
+    }
+    bool same = true;
+#pragma unroll
+    for (int j = 0; j < NHL; ++j) same &= sc[j] == 1.f;
+    if (!__all_sync(0xffffffffu, same)) {
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        O[mt][0] *= sc[0];
+        O[mt][2] *= sc[0];
+        O[mt][1] *= sc[NHL - 1];
+        O[mt][3] *= sc[NHL - 1];
+      }
+    }
+    // B operand P^T: lane holds P[rows 2 t4, 2 t4 + 1][column g8] (rows 8..15 do not exist);
+    // (row r, lane head slot) lives in lane r * 4 + head slot
+    const int src0 = (2 * t4) * 4 + (g8 >> 1), src1 = src0 + 4;
+    uint32_t pb, pl = 0u;
+    if (kSplitCols) {
+      const float v0 = __shfl_sync(0xffffffffu, pr[0], src0);
+      const float v1 = __shfl_sync(0xffffffffu, pr[0], src1);
+      const bool lo = g8 & 1;
+      pb = pack_bf16(lo ? bf16_lo(v0) : v0, lo ? bf16_lo(v1) : v1);
+    } else {
+      const bool odd = g8 & 1;  // column g8 = head; element j = head & 1 of the source lane
+      const float a0 = __shfl_sync(0xffffffffu, pr[0], src0), b0 = __shfl_sync(0xffffffffu, pr[NHL - 1], src0);
+      const float a1 = __shfl_sync(0xffffffffu, pr[0], src1), b1 = __shfl_sync(0xffffffffu, pr[NHL - 1], src1);
+      const float v0 = odd ? b0 : a0, v1 = odd ? b1 : a1;
+      pb = pack_bf16(v0, v1);
+      pl = pack_bf16(bf16_lo(v0), bf16_lo(v1));
+    }
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      const int dim = 16 * mt + (cX << 3);
+      uint32_t a2[2];
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                   : "=r"(a2[0]), "=r"(a2[1])
+                   : "r"(swz128(sb + (NH + (dim >> 6)) * HW, rX, (dim & 63) >> 3)));
+      const uint32_t a[4] = {a2[0], a2[1], 0u, 0u};
+      mma_bf16(O[mt], a, pb, 0u);
+      if (!kSplitCols) mma_bf16(O[mt], a, pl, 0u);
+    }
+    __syncwarp();
+    if (k + nsw < mine) issue(k + nsw, rp);
+  }
+#pragma unroll
+  for (int j = 0; j < NHL; ++j) {
+    l[j] += __shfl_xor_sync(0xffffffffu, l[j], 4);
+    l[j] += __shfl_xor_sync(0xffffffffu, l[j], 8);
+    l[j] += __shfl_xor_sync(0xffffffffu, l[j], 16);
+  }
+  __syncthreads();  // wpart aliases the ring: every warp has drained its slots
+#pragma unroll
+  for (int j = 0; j < NHL; ++j) {
+    const int head = kSplitCols ? t4 : 2 * t4 + j;
+    if (head < G) {
+      float* dstp = wpart + ((size_t)w * G_T + head) * (D_T + 2);
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        if (kSplitCols) {
+          dstp[16 * mt + g8] = O[mt][0] + O[mt][1];
+          dstp[16 * mt + g8 + 8] = O[mt][2] + O[mt][3];
+        } else {
+          dstp[16 * mt + g8] = O[mt][j];
+          dstp[16 * mt + g8 + 8] = O[mt][2 + j];
+        }
+      }
+      if (g8 == 0) {
+        dstp[D_T] = m[j];
+        dstp[D_T + 1] = l[j];
+      }
+    }
   }
 }
 
@@ -692,145 +1154,17 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   }
   __syncthreads();
 
-  const int kcol0 = split ? p.d : 0;  // first gathered K column
-  const int KW = D - kcol0;           // gathered K columns
-  const int KROWB = KW * E;
-  const int R3 = p.r3;
-  const int nstage = ceil_div(n, R3);
-  const unsigned stage_bytes = (unsigned)(R3 * (KROWB + ROWB));
-  const bool want_logits = p.weights_out != nullptr;
-  const int row_base = (int)(((long long)b * p.Hkv + hk) * p.unit_rows);
-  const int mine = nstage > w ? ceil_div(nstage - w, kPW) : 0;  // stages w, w + kPW, ...
-  auto issue = [&](int k, const RingPos& at) {
-    const int st = w + k * kPW;
-    uint8_t* dst = wring + at.slot * SB;
-    if (lane == 0) mbar_expect_tx(&wbar[at.slot], stage_bytes);
-    int row = -1;  // lane t < R3 resolves row t of the stage; -1 = out of bounds, zero-filled
-    const int t = st * R3 + lane;
-    if (lane < R3 && t < n) row = row_base + (int)(ents[t] & 0xFFFFFFu);
-    for (int qq = 0; qq < R3 / 4; ++qq) {
-      const int a0 = __shfl_sync(0xffffffffu, row, 4 * qq);
-      const int a1 = __shfl_sync(0xffffffffu, row, 4 * qq + 1);
-      const int a2 = __shfl_sync(0xffffffffu, row, 4 * qq + 2);
-      const int a3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
-      if (lane == 0) {
-        tma_gather4(dst + qq * 4 * KROWB, krow_map, kcol0, a0, a1, a2, a3, &wbar[at.slot]);
-        tma_gather4(dst + R3 * KROWB + qq * 4 * ROWB, vrow_map, 0, a0, a1, a2, a3, &wbar[at.slot]);
-      }
-    }
-  };
-  {
-    RingPos qp = rp;
-    for (int k = 0; k < nsw && k < mine; ++k, qp.advance(1)) issue(k, qp);
-  }
-  float acc[G_T][VEC];
-  float m[G_T], l[G_T];
-#pragma unroll
-  for (int g = 0; g < G_T; ++g) {
-    m[g] = -CUDART_INF_F;
-    l[g] = 0.f;
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[g][v] = 0.f;
-  }
-  const int r = lane / LPR3, sl = lane % LPR3;
-  const bool k_on = sl * VEC < KW;
-  float q3[G_T][VEC];
-#pragma unroll
-  for (int g = 0; g < G_T; ++g)
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const int col = kcol0 + sl * VEC + v;
-      q3[g][v] = (g < G && k_on && col < D) ? p.q_hat[(qrow0 + g) * D + col] * p.qscale : 0.f;
-    }
-  constexpr int U = 2;  // rows per lane slot whose logits are formed before the softmax updates
-  for (int k = 0; k < mine; ++k, rp.advance(1)) {
-    mbar_wait(&wbar[rp.slot], rp.phase);
-    const int st = w + k * kPW;
-    const uint8_t* kt = wring + rp.slot * SB;
-    const uint8_t* vt = kt + R3 * KROWB;
-    for (int ps = 0; ps < R3 / RPW3; ps += U) {  // host: (R3 / RPW3) % U == 0
-      float x[U][G_T];
-      int jr[U];
-      unsigned msk[U];
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        const int rr = (ps + uu) * RPW3 + r;
-        const int t = st * R3 + rr;
-        const bool ok = t < n;
-        const uint32_t e = ok ? ents[t] : 0u;
-        jr[uu] = (int)(e & 0xFFFFFFu);
-        msk[uu] = e >> 24;
-        float kx[VEC];
-        if (k_on) lds_chunk<T, VEC>(kt + rr * KROWB + sl * VEC * E, kx);
-        else
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) kx[v] = 0.f;
-#pragma unroll
-        for (int g = 0; g < G_T; ++g) {
-          float s = 0.f;
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) s = fmaf(q3[g][v], kx[v], s);
-          s = sum_lanes<LPR3>(s);
-          if (split && ok && g < G) s += apx[g * p.Lc + t];
-          x[uu][g] = s;
-        }
-      }
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        const int rr = (ps + uu) * RPW3 + r;
-        float vx[VEC];
-        lds_chunk<T, VEC>(vt + rr * ROWB + sl * VEC * E, vx);
-#pragma unroll
-        for (int g = 0; g < G_T; ++g) {
-          if (msk[uu] & (1u << g)) {
-            const float xv = x[uu][g];
-            if (want_logits && sl == 0) p.logits[((size_t)u * G + g) * p.S_cap + jr[uu]] = xv;
-            const float mn = fmaxf(m[g], xv);
-            const float sc = exp2f(m[g] - mn);
-            const float pe = exp2f(xv - mn);
-            l[g] = l[g] * sc + pe;
-            m[g] = mn;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[g][v] = fmaf(pe, vx[v], acc[g][v] * sc);
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (k + nsw < mine) issue(k + nsw, rp);
-  }
-
-  // merge lanes sharing columns, then warps in fixed order, into this part's state
-#pragma unroll
-  for (int g = 0; g < G_T; ++g) {
-    for (int off = LPR3; off < 32; off <<= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m[g], off);
-      const float l2 = __shfl_xor_sync(0xffffffffu, l[g], off);
-      float s1, s2;
-      merge_state(m[g], l[g], m2, l2, s1, s2);
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        const float a2 = __shfl_xor_sync(0xffffffffu, acc[g][v], off);
-        acc[g][v] = acc[g][v] * s1 + a2 * s2;
-      }
-    }
-  }
   const int ldp = D + 2;
   float* wpart = reinterpret_cast<float*>(ring);  // [kPW][G_T][D + 2]; every ring slot has been consumed
-  __syncthreads();
-  if (r == 0) {
-#pragma unroll
-    for (int g = 0; g < G_T; ++g) {
-      if (g >= G) break;
-      float* dstp = wpart + ((size_t)w * G_T + g) * ldp;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) dstp[sl * VEC + v] = acc[g][v];
-      if (sl == 0) {
-        dstp[D] = m[g];
-        dstp[D + 1] = l[g];
-      }
+  const int row_base = (int)(((long long)b * p.Hkv + hk) * p.unit_rows);
+  bool done = false;
+  if constexpr (sizeof(T) == 2) {
+    if (p.mma) {
+      stream_B_mma<G_T, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, wring, wbar, rp, wpart);
+      done = true;
     }
   }
+  if (!done) stream_B_simt<T, G_T, VEC, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, apx, wring, wbar, rp, wpart);
   __syncthreads();
   float* gpart = p.part + (((size_t)u * p.nA + q) * G) * ldp;
   for (int i = tid; i < G * ldp; i += kPT) {
@@ -859,12 +1193,14 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
 
 // ------------------------------------------------------------------ kernel
 template <typename T, int G_T, int VEC, int D_T>
-__global__ void __launch_bounds__(kPT) pipe_decode_kernel(const PipeParams p,
+__global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
                                                           const __grid_constant__ CUtensorMap lead_map,
                                                           const __grid_constant__ CUtensorMap krow_map,
                                                           const __grid_constant__ CUtensorMap vrow_map) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ PipeShared sh;
+  // 1024 B alignment: the tensor-core path reads 128B-swizzled TMA tiles
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int nsw = p.nst;
   uint8_t* ring = smem + p.off_ring;
@@ -939,6 +1275,7 @@ size_t pipe_layout(int G_T, PipeParams* p) {
   off = align_up(off + (size_t)G_T * (1u << hb) * 4, 16);
   p->off_ents = (int)off;
   off = align_up(off + (size_t)p->Lc * 4 * (1 + (p->split_k ? G_T : 0)), 128);
+  off += 1024;  // slack for aligning the dynamic shared memory base to 1024 B
   p->cand_cap = (int)((size_t)kPW * p->nst * p->stage_bytes / 24);  // three u64 candidate buffers
   return off;
 }
