@@ -217,30 +217,94 @@ __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
   return x - v;
 }
 
+// Keys of one head streamed through shared memory: two buffers of kCK keys
+// filled by cp.async.bulk (one L2 round trip per chunk, the next chunk in
+// flight while this one is scanned).  `sbar` are two mbarriers owned by the
+// selection; `sphase` holds their parity bits (identical in every thread).
+constexpr int kCK = 4096;  // keys per chunk (16 KB)
+
+struct KeyStream {
+  const uint32_t* src;
+  int S, kstride;
+  uint32_t* buf;  // [2][kCK]
+  uint64_t* sbar;
+  unsigned* sphase;
+  int nchunk;
+  __device__ void issue(int c) const {
+    if (threadIdx.x == 0 && c < nchunk) {
+      const int base = c * kCK;
+      int rows = min(kCK, kstride - base);
+      const unsigned bytes = (unsigned)(((rows * 4) + 15) & ~15);
+      uint64_t* bar = &sbar[c & 1];
+      mbar_expect_tx(bar, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(buf + (c & 1) * kCK)),
+          "l"(src + base), "r"(bytes), "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  // chunks 0 and 1 in flight (call once per pass, before run)
+  __device__ void start() const {
+    if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // keys were stored by generic st
+    issue(0);
+    issue(1);
+  }
+  // wait for the chunks start() issued without reading them
+  __device__ void drain() const {
+    for (int c = 0; c < 2 && c < nchunk; ++c) {
+      mbar_wait(&sbar[c], (*sphase >> c) & 1u);
+      *sphase ^= 1u << c;
+    }
+    __syncthreads();
+  }
+  // f(j0, keys, n): rows [j0, j0 + n) of the chunk in shared memory; every thread calls
+  template <typename F>
+  __device__ void run(F&& f) const {
+    for (int c = 0; c < nchunk; ++c) {
+      const int bi = c & 1;
+      mbar_wait(&sbar[bi], (*sphase >> bi) & 1u);
+      *sphase ^= 1u << bi;
+      f(c * kCK, buf + bi * kCK, min(kCK, S - c * kCK));
+      __syncthreads();  // every thread is done with buffer bi before it is refilled
+      issue(c + 2);
+    }
+  }
+};
+
+// LOKI_DEBUG & 16 (tuning only): %globaltimer at selection checkpoints, [units][8] at trace + 2^21
+__device__ __forceinline__ void sel_stamp(const PipeParams& p, int u, int k) {
+  if ((p.debug & 16) && p.trace != nullptr && threadIdx.x == 0) p.trace[(1 << 21) + (size_t)u * 8 + k] = globaltimer();
+}
+
 // Threshold of each head's top-k in unit u on 64-bit composite keys: the
 // last A arriver reads the level-0 histogram, compacts the boundary-bin rows
-// into shared memory with one L2 scan (further histogram levels only if they
-// do not fit), narrows them (radix passes, then a direct rank once <= 256
-// remain) and publishes tcs[u][g].  With idx_out it also publishes each
-// part's output offset (rows above the boundary per part + candidates kept).
+// into shared memory with one pass over the keys (further histogram levels
+// only if they do not fit), narrows them (radix passes, then a direct rank
+// once <= 256 remain) and publishes tcs[u][g].  With idx_out it also
+// publishes each part's output offset (rows above the boundary per part +
+// candidates kept).
 template <int G_T>
-__device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem, uint32_t* hist, PipeShared& sh) {
+__device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, uint32_t* hist, uint64_t* sbar,
+                            unsigned& sphase, PipeShared& sh) {
   const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int G = p.G, hb = p.hbits, HB = 1 << hb;
   uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
   const int kb = k_of(p, S);
   const int cap = p.cand_cap;
   const bool offsets = p.idx_out != nullptr;
-  unsigned long long* candA = reinterpret_cast<unsigned long long*>(cand_mem);
+  uint32_t* kbuf = reinterpret_cast<uint32_t*>(ring);
+  unsigned long long* candA = reinterpret_cast<unsigned long long*>(ring + 2 * kCK * 4);
   unsigned long long* candB = candA + cap;
   unsigned long long* candC = candB + cap;
-  const int Rw = ceil_div(ceil_div(S > 0 ? S : 1, kPW), 128) * 128;
-  const int ra = min(w * Rw, S), rb = min(ra + Rw, S);
   const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
   for (int g = 0; g < G; ++g) {
     const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
     uint32_t* gh = p.hist + ((size_t)u * G + g) * HB;
     uint32_t* poff = offsets ? p.poff + ((size_t)u * G + g) * p.nA : nullptr;
+    KeyStream ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
+    if (g == 0) sel_stamp(p, u, 0);
+    if (kb > 0) ks.start();  // speculative: the compaction pass below almost always runs
     for (int i = tid; i < HB; i += kPT) {
       hist[i] = __ldcg(&gh[i]);
       gh[i] = 0u;  // ready for the next launch
@@ -253,55 +317,77 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem
       continue;
     }
     find_bin(hist, HB, (unsigned)kb, sh);
+    if (g == 0) sel_stamp(p, u, 1);
     unsigned long long P = (unsigned long long)sh.fb_bin;
     int nb = hb;
     unsigned need = (unsigned)kb - sh.fb_above, cnt = sh.fb_cnt;
     int ncand = 0;
-    bool listed = false;
+    bool listed = false, started = true;
     for (;;) {
+      if (!started) ks.start();
+      started = false;
       if (cnt <= (unsigned)cap) {  // compact the rows matching P (and count the rows above P per part)
         if (tid == 0) sh.ncand = 0;
         __syncthreads();
         const unsigned long long Pc = P;
         const int sh64 = 64 - nb;
-        scan_rows(keys, ra, rb, [&](int jb, const uint4& kk) {
-          int above = 0;
+        ks.run([&](int j0, const uint32_t* kc, int nrow) {
+          for (int i0 = 0; i0 < nrow; i0 += 4 * kPT) {
+            const int il = i0 + 4 * tid;
+            const uint4 kk = *reinterpret_cast<const uint4*>(kc + il);
+            int above = 0;
+            bool any = false;
+            if (nb <= 32) {  // prefix inside the 32-bit key: cheap tests, composites only for candidates
+              const int s32 = 32 - nb;
+              const uint32_t P32 = (uint32_t)Pc;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = jb + e;
-            const unsigned long long c = comp_key(u4_at(kk, e), j);
-            const bool ok = j < rb;
-            above += (ok && (c >> sh64) > Pc) ? 1 : 0;
-            append_if(ok && (c >> sh64) == Pc, c, candA, &sh.ncand);
-          }
-          if (offsets) {  // a 128-row block lies inside one part (Lc % 128 == 0)
-            above = __reduce_add_sync(0xffffffffu, above);
-            const int j0 = __shfl_sync(0xffffffffu, jb, 0);
-            if (lane == 0 && above) atomicAdd(&poff[j0 / p.Lc], (uint32_t)above);
+              for (int e = 0; e < 4; ++e) {
+                const bool ok = il + e < nrow;
+                const uint32_t pre = u4_at(kk, e) >> s32;
+                above += (ok && pre > P32) ? 1 : 0;
+                any |= ok && pre == P32;
+              }
+            } else {
+              any = true;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                above += (il + e < nrow && (comp_key(u4_at(kk, e), j0 + il + e) >> sh64) > Pc) ? 1 : 0;
+            }
+            if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const unsigned long long c = comp_key(u4_at(kk, e), j0 + il + e);
+                append_if(il + e < nrow && (c >> sh64) == Pc, c, candA, &sh.ncand);
+              }
+            }
+            if (offsets) {  // a warp's 128 rows lie inside one part (Lc % 128 == 0)
+              above = __reduce_add_sync(0xffffffffu, above);
+              const int jw = j0 + i0 + 128 * w;
+              if (lane == 0 && above) atomicAdd(&poff[jw / p.Lc], (uint32_t)above);
+            }
           }
         });
-        __syncthreads();
         ncand = sh.ncand;
         if (tid == 0) sh.ncand_first = ncand;
         listed = true;
         break;
       }
-      if (cnt == need) break;
+      if (cnt == need) {  // exact boundary bin, too large to list: drain the prefetched chunks
+        ks.drain();
+        break;
+      }
       // one more histogram level over every row matching P
       const int bits = min(hb, 64 - nb);
       for (int i = tid; i < (1 << bits); i += kPT) hist[i] = 0u;
       __syncthreads();
       const unsigned long long Pc = P;
       const int sh64 = 64 - nb;
-      scan_rows(keys, ra, rb, [&](int jb, const uint4& kk) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = jb + e;
-          const unsigned long long c = comp_key(u4_at(kk, e), j);
-          if (j < rb && (c >> sh64) == Pc) atomicAdd(&hist[(c >> (sh64 - bits)) & ((1ull << bits) - 1)], 1u);
+      ks.run([&](int j0, const uint32_t* kc, int nrow) {
+        for (int i = tid; i < nrow; i += kPT) {
+          const unsigned long long c = comp_key(kc[i], j0 + i);
+          if ((c >> sh64) == Pc) atomicAdd(&hist[(c >> (sh64 - bits)) & ((1ull << bits) - 1)], 1u);
         }
       });
-      __syncthreads();
       find_bin(hist, 1 << bits, need, sh);
       P = (P << bits) | (unsigned long long)sh.fb_bin;
       nb += bits;
@@ -309,6 +395,8 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem
       cnt = sh.fb_cnt;
     }
     unsigned long long Tc;
+    if (g == 0) sel_stamp(p, u, 2);
+    if ((p.debug & 16) && p.trace != nullptr && tid == 0 && g == 0) p.trace[(1 << 21) + (size_t)u * 8 + 7] = ncand;
     if (listed) {  // narrow inside shared memory; candA stays intact for the part counts
       const unsigned long long* src = candA;
       unsigned long long* dst = candB;
@@ -337,6 +425,7 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem
         src = dst;
         dst = (dst == candB) ? candC : candB;
       }
+      if (g == 0) sel_stamp(p, u, 3);
       if (cnt == need) {
         Tc = nb >= 64 ? P : (P << (64 - nb));
       } else {  // <= 256 distinct candidates: the need-th largest by direct rank
@@ -358,16 +447,19 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem
       }
     } else {
       Tc = nb >= 64 ? P : (P << (64 - nb));
-      if (offsets)  // counting pass: rows >= Tc per part
-        scan_rows(keys, ra, rb, [&](int jb, const uint4& kk) {
-          int c = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) c += (jb + e < rb && comp_key(u4_at(kk, e), jb + e) >= Tc) ? 1 : 0;
-          c = __reduce_add_sync(0xffffffffu, c);
-          const int j0 = __shfl_sync(0xffffffffu, jb, 0);
-          if (lane == 0 && c) atomicAdd(&poff[j0 / p.Lc], (uint32_t)c);
+      if (offsets) {  // counting pass: rows >= Tc per part
+        ks.start();
+        ks.run([&](int j0, const uint32_t* kc, int nrow) {
+          for (int i0 = 0; i0 < nrow; i0 += kPT) {
+            const int i = i0 + tid;
+            const bool on = i < nrow && comp_key(kc[i], j0 + i) >= Tc;
+            const int c = __popc(__ballot_sync(0xffffffffu, on));
+            if (lane == 0 && c) atomicAdd(&poff[(j0 + i0 + 32 * w) / p.Lc], (uint32_t)c);
+          }
         });
+      }
     }
+    if (g == 0) sel_stamp(p, u, 4);
     if (tid == 0) p.tcs[(size_t)u * G + g] = Tc;
     if (offsets) {  // counts -> exclusive offsets (one warp)
       __syncthreads();
@@ -390,9 +482,13 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* cand_mem
     __syncthreads();
   }
   if (tid == 0) cu[0] = 0u;  // A arrivals: ready for the next launch
-  __threadfence();
+  sel_stamp(p, u, 5);
   __syncthreads();
-  if (tid == 0) st_release(&cu[2], 1u);
+  if (tid == 0) {  // the barrier makes every thread's writes visible to thread 0; its release publishes them
+    __threadfence();
+    st_release(&cu[2], 1u);
+  }
+  sel_stamp(p, u, 6);
 }
 
 // ------------------------------------------------------------------ item A
@@ -503,7 +599,8 @@ __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint
 
 template <typename T, int G_T, int VEC>
 __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, int c, uint8_t* ring,
-                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, RingPos& rp, PipeShared& sh) {
+                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, uint64_t* sbar, unsigned& sphase, RingPos& rp,
+                       PipeShared& sh) {
   constexpr int E = sizeof(T);
   const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int nsw = p.nst, SB = p.stage_bytes;
@@ -595,14 +692,16 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
     const uint32_t v = hist[i];
     if (v) atomicAdd(&gh[i], v);
   }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) sh.last = atomicAdd(&p.ctrl[2 + 4 * (size_t)u], 1u) == (unsigned)nparts - 1u;
+  if (tid == 0) {
+    __threadfence();
+    sh.last = atomicAdd(&p.ctrl[2 + 4 * (size_t)u], 1u) == (unsigned)nparts - 1u;
+    if (sh.last) __threadfence();
+  }
   __syncthreads();
   if (sh.last) {
-    __threadfence();
     if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();
-    select_unit<G_T>(p, u, S, ring, hist, sh);
+    select_unit<G_T>(p, u, S, ring, hist, sbar, sphase, sh);
     return 3;
   }
   return 1;
@@ -1178,12 +1277,14 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
     }
     gpart[(size_t)g * ldp + col] = col < D ? aa : (col == D ? mm : ll);
   }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) sh.last = atomicAdd(&cu[1], 1u) == (unsigned)nparts - 1u;
+  if (tid == 0) {
+    __threadfence();
+    sh.last = atomicAdd(&cu[1], 1u) == (unsigned)nparts - 1u;
+    if (sh.last) __threadfence();
+  }
   __syncthreads();
   if (sh.last) {
-    __threadfence();
     if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();
     merge_unit<G_T>(p, u, S, sh);
     return 4;
@@ -1208,8 +1309,14 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
   uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bars) + (size_t)w * nsw;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + p.off_hist);
   uint32_t* ents = reinterpret_cast<uint32_t*>(smem + p.off_ents);
+  uint64_t* sbar = reinterpret_cast<uint64_t*>(smem + p.off_bars) + (size_t)kPW * nsw;  // selection key stream
+  unsigned sphase = 0u;
   if (lane == 0) {
     for (int s = 0; s < nsw; ++s) mbar_init(&wbar[s], 1);
+    if (w == 0) {
+      mbar_init(&sbar[0], 1);
+      mbar_init(&sbar[1], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (tid == 0) {
@@ -1238,7 +1345,8 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
     const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
     int kind = 0;
     if (r < p.nA) {
-      if (slot < p.units) kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, rp, sh);
+      if (slot < p.units)
+        kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, sbar, sphase, rp, sh);
     } else {
       const int u = slot - p.lag;
       if (u >= 0 && u < p.units)
@@ -1269,14 +1377,16 @@ size_t pipe_layout(int G_T, PipeParams* p) {
   p->off_ring = 0;
   off += (size_t)kPW * p->nst * p->stage_bytes;
   p->off_bars = (int)off;
-  off = align_up(off + (size_t)kPW * p->nst * 8, 16);
+  off = align_up(off + (size_t)(kPW * p->nst + 2) * 8, 16);
   p->off_hist = (int)off;
   const int hb = p->hbits > 8 ? p->hbits : 8;
   off = align_up(off + (size_t)G_T * (1u << hb) * 4, 16);
   p->off_ents = (int)off;
   off = align_up(off + (size_t)p->Lc * 4 * (1 + (p->split_k ? G_T : 0)), 128);
   off += 1024;  // slack for aligning the dynamic shared memory base to 1024 B
-  p->cand_cap = (int)((size_t)kPW * p->nst * p->stage_bytes / 24);  // three u64 candidate buffers
+  // ring during a selection: two key chunks of kCK keys, then three u64 candidate buffers
+  const long long rest = (long long)kPW * p->nst * p->stage_bytes - 2LL * kCK * 4;
+  p->cand_cap = rest > 0 ? (int)(rest / 24) : 0;
   return off;
 }
 

@@ -63,7 +63,7 @@ if os.environ.get("LOKI_TRACE") and call.plan()["ctas_per_unit"] == 0:
     # persistent pipe kernel: per-ticket {start, end, smid | kind << 16 | block << 32}
     import numpy as np
 
-    nbuf = 1 << 22
+    nbuf = 1 << 23
     buf = torch.zeros(nbuf, dtype=torch.int64, device=dev)
     lib = _lib.load()
     _lib.check(lib.loki_set_phase_trace(buf.data_ptr(), nbuf // 8))
@@ -93,6 +93,15 @@ if os.environ.get("LOKI_TRACE") and call.plan()["ctas_per_unit"] == 0:
     occA = [((st <= x) & (en > x) & (ab == 1)).sum() for x in grid]
     occB = [((st <= x) & (en > x) & (bb_ == 1)).sum() for x in grid]
     print("  CTAs in A / B over time:", " ".join(f"{a}/{b}" for a, b in zip(occA, occB)))
+    if int(os.environ.get("LOKI_DEBUG", "0")) & 16:
+        st8 = buf.view(-1).cpu().numpy()[1 << 21:(1 << 21) + a.B * a.Hkv * 8].reshape(-1, 8)
+        ok = st8[:, 0] != 0
+        st8 = st8[ok]
+        names = ["hist+find_bin", "compaction", "narrow", "rank", "offsets/misc", "fence+release"]
+        for i, nm in enumerate(names):
+            dd = (st8[:, i + 1] - st8[:, i]) / 1e3
+            print(f"    sel {nm:14s} median {np.median(dd):6.2f} us  max {dd.max():6.2f}")
+        print(f"    sel ncand median {np.median(st8[:, 7]):.0f} max {st8[:, 7].max()}")
     blk = t[:, 2] >> 32
     idle = []
     for bb in np.unique(blk):
