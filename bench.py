@@ -160,10 +160,14 @@ class Workload:
         self.cfg = cfg
         self.world, self.rank = world, rank
         L, B, Hq, Hkv, D, S = (cfg[k] for k in ("layers", "B", "Hq", "Hkv", "D", "S"))
-        if Hkv % world:
-            raise SystemExit(f"{Hkv} KV heads cannot be sharded over {world} GPUs")
-        self.Hkv_l = Hkv // world
-        self.Hq_l = Hq // world
+        from paper_2406_02542_b200 import sharding
+
+        try:
+            self.shard = sharding.head_shard(Hq, Hkv, world, rank)
+        except Exception as e:  # uneven split: the config cannot run at this world size
+            raise SystemExit(str(e))
+        self.Hkv_l = self.shard.kv_heads
+        self.Hq_l = self.shard.q_heads
         self.G = Hq // Hkv
         self.L, self.B, self.D, self.S = L, B, D, S
         self.d = max(1, min(D, math.floor(cfg["d_f"] * D + 0.5)))
@@ -215,7 +219,8 @@ class Workload:
         self.lens = torch.full((B,), S, dtype=torch.int32, device=dev)
         self.positions = torch.full((B,), S - 1, dtype=torch.int64, device=dev)
         self.out = torch.empty(L, B, self.Hq_l, D, device=dev)
-        self.gathered = torch.empty(L, world, B, self.Hq_l, D, device=dev) if world > 1 else None
+        self.gathered = torch.empty(L, world * B, self.Hq_l, D, device=dev) if world > 1 else None
+        self.full_out = torch.empty(L, B, Hq, D, device=dev) if world > 1 else None
 
     def decoders(self, dense=False):
         from paper_2406_02542_b200 import LokiDecoder, _lib
@@ -231,9 +236,11 @@ class Workload:
 
 
 def gather_outputs(wl, layer, stream_ctx=None):
-    import torch.distributed as dist
+    """The one exchange step of a head-sharded layer: NCCL all-gather of the
+    per-rank [B, Hq/world, D] outputs into [B, Hq, D] for the next layer."""
+    from paper_2406_02542_b200 import sharding
 
-    dist.all_gather_into_tensor(wl.gathered[layer], wl.out[layer])
+    sharding.gather_heads(wl.out[layer], wl.world, out=wl.full_out[layer], staging=wl.gathered[layer])
 
 
 def make_step(wl, decs, world, attend_only=False):
