@@ -315,9 +315,9 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   pl->off_tcs = off;
   off = loki::align_up(off + (size_t)units * G * 8, 256);
   pl->off_poff = off;
-  if (a->idx_out != nullptr) off = loki::align_up(off + (size_t)units * G * p.nA * 4, 256);
+  if (a->idx_out != nullptr) off = loki::align_up(off + (size_t)units * G * 2 * p.nA * 4, 256);
   pl->off_part = off;
-  off = loki::align_up(off + (size_t)units * p.nA * G * (g.D + 2) * 4, 256);
+  off = loki::align_up(off + (size_t)units * 2 * p.nA * G * (g.D + 2) * 4, 256);  // full or half parts
   pl->off_logits = off;
   if (a->weights_out != nullptr) off = loki::align_up(off + (size_t)units * G * g.S_cap * 4, 256);
   pl->ws = off;

@@ -79,8 +79,8 @@ struct PipeParams {
   uint32_t* keys;    // [units][G][kstride] order keys of the approx scores
   int kstride;       // S_cap rounded up to a multiple of 4 (uint4 scans)
   unsigned long long* tcs;  // [units][G] selection thresholds on composite keys
-  uint32_t* poff;    // [units][G][nA] idx_out offset of each part (idx_out only)
-  float* part;       // [units][nA][G][D + 2] per-part (acc[D], m, l)
+  uint32_t* poff;    // [units][G][2 nA] idx_out offset of each half part (idx_out only)
+  float* part;       // [units][2 nA][G][D + 2] per-part (acc[D], m, l); tail units use half parts
   float* logits;     // [units][G][S_cap] exact logits (weights_out only) or null
   long long* trace;  // optional [n_tickets][4] {start, end, sm | kind << 16 | block << 32, tail start}
   int debug;

@@ -297,11 +297,12 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
   unsigned long long* candA = reinterpret_cast<unsigned long long*>(ring + 2 * kCK * 4);
   unsigned long long* candB = candA + cap;
   unsigned long long* candC = candB + cap;
-  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
+  const int Lh = p.Lc / 2;                      // idx_out offsets at half-part granularity
+  const int nhp = ceil_div(S > 0 ? S : 1, Lh);
   for (int g = 0; g < G; ++g) {
     const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
     uint32_t* gh = p.hist + ((size_t)u * G + g) * HB;
-    uint32_t* poff = offsets ? p.poff + ((size_t)u * G + g) * p.nA : nullptr;
+    uint32_t* poff = offsets ? p.poff + ((size_t)u * G + g) * 2 * p.nA : nullptr;  // per half part
     KeyStream ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
     if (g == 0) sel_stamp(p, u, 0);
     if (kb > 0) ks.start();  // speculative: the compaction pass below almost always runs
@@ -310,7 +311,7 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
       gh[i] = 0u;  // ready for the next launch
     }
     if (offsets)
-      for (int q = tid; q < nparts; q += kPT) poff[q] = 0u;
+      for (int q = tid; q < nhp; q += kPT) poff[q] = 0u;
     __syncthreads();
     if (kb == 0) {
       if (tid == 0) p.tcs[(size_t)u * G + g] = ~0ull;
@@ -360,10 +361,10 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
                 append_if(il + e < nrow && (c >> sh64) == Pc, c, candA, &sh.ncand);
               }
             }
-            if (offsets) {  // a warp's 128 rows lie inside one part (Lc % 128 == 0)
+            if (offsets) {  // a warp's 128 rows lie inside one half part (Lc / 2 % 128 == 0)
               above = __reduce_add_sync(0xffffffffu, above);
               const int jw = j0 + i0 + 128 * w;
-              if (lane == 0 && above) atomicAdd(&poff[jw / p.Lc], (uint32_t)above);
+              if (lane == 0 && above) atomicAdd(&poff[jw / Lh], (uint32_t)above);
             }
           }
         });
@@ -442,7 +443,7 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
         const int n0 = sh.ncand_first;
         for (int i = tid; i < n0; i += kPT) {
           const unsigned long long c = candA[i];
-          if (c >= Tc) atomicAdd(&poff[(int)(~(uint32_t)c) / p.Lc], 1u);
+          if (c >= Tc) atomicAdd(&poff[(int)(~(uint32_t)c) / Lh], 1u);
         }
       }
     } else {
@@ -454,7 +455,7 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
             const int i = i0 + tid;
             const bool on = i < nrow && comp_key(kc[i], j0 + i) >= Tc;
             const int c = __popc(__ballot_sync(0xffffffffu, on));
-            if (lane == 0 && c) atomicAdd(&poff[(j0 + i0 + 32 * w) / p.Lc], (uint32_t)c);
+            if (lane == 0 && c) atomicAdd(&poff[(j0 + i0 + 32 * w) / Lh], (uint32_t)c);
           }
         });
       }
@@ -465,16 +466,16 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
       __syncthreads();
       if (w == 0) {
         unsigned run = 0;
-        for (int q0 = 0; q0 < nparts; q0 += 32) {
+        for (int q0 = 0; q0 < nhp; q0 += 32) {
           const int q = q0 + lane;
-          const unsigned v = q < nparts ? __ldcg(&poff[q]) : 0u;
+          const unsigned v = q < nhp ? __ldcg(&poff[q]) : 0u;
           unsigned x = v;
 #pragma unroll
           for (int off = 1; off < 32; off <<= 1) {
             const unsigned t = __shfl_up_sync(0xffffffffu, x, off);
             if (lane >= off) x += t;
           }
-          if (q < nparts) poff[q] = run + x - v;
+          if (q < nhp) poff[q] = run + x - v;
           run += __shfl_sync(0xffffffffu, x, 31);
         }
       }
@@ -714,8 +715,9 @@ __device__ void merge_unit(const PipeParams& p, int u, int S, PipeShared& sh) {
   const int G = p.G, D = p.D, ldp = D + 2;
   uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
   const size_t qrow0 = ((size_t)(u / p.Hkv) * p.Hq) + (size_t)(u % p.Hkv) * G;
-  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
-  const float* part = p.part + (size_t)u * p.nA * G * ldp;
+  const bool split = u + p.lag >= p.units;  // tail units run half-size B items
+  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc) * (split ? 2 : 1);
+  const float* part = p.part + (size_t)u * 2 * p.nA * G * ldp;
   for (int i = tid; i < G * D; i += kPT) {
     const int g = i / D, col = i % D;
     float mm = -CUDART_INF_F, ll = 0.f, aa = 0.f;
@@ -1116,7 +1118,8 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
 // B(u, q): rows [q * Lc, (q + 1) * Lc).  kNB 128-row blocks per warp.
 template <typename T, int G_T, int VEC, int D_T>
 __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u, int q,
-                       uint8_t* ring, uint8_t* wring, uint64_t* wbar, uint32_t* ents, RingPos& rp, PipeShared& sh) {
+                      int half, uint8_t* ring, uint8_t* wring, uint64_t* wbar, uint32_t* ents, RingPos& rp,
+                      PipeShared& sh) {
   constexpr int E = sizeof(T);
   constexpr int LPR3 = D_T / VEC;  // lanes per V row
   constexpr int RPW3 = 32 / LPR3;
@@ -1129,8 +1132,12 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
   const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
   if (q >= nparts) return 0;  // past this unit's length: not an arrival
-  const int row0 = q * p.Lc;
-  const int nrows = max(0, min(S - row0, p.Lc));
+  // full part q = rows [q Lc, (q + 1) Lc); the tail units' half parts (half = 0 / 1) cover Lc / 2 rows each
+  const int span = half < 0 ? p.Lc : p.Lc / 2;
+  const int row0 = q * p.Lc + (half > 0 ? span : 0);
+  const int nrows = max(0, min(S - row0, span));
+  const int pidx = half < 0 ? q : 2 * q + half;             // partial-state slot
+  const int narrive = half < 0 ? nparts : 2 * nparts;     // B items of this unit
   uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
   if (tid == 0) {
     unsigned long long spins = 0;
@@ -1233,7 +1240,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
 #pragma unroll
       for (int g = 0; g < G_T; ++g) {
         if (g >= G) break;
-        int base = (int)__ldcg(&p.poff[((size_t)u * G + g) * p.nA + q]);
+        int base = (int)__ldcg(&p.poff[((size_t)u * G + g) * 2 * p.nA + row0 / (p.Lc / 2)]);
         for (int ww = 0; ww < w; ++ww) base += sh.wcnt[ww][1 + g];
         int32_t* dst = p.idx_out + (qrow0 + g) * p.idx_stride;
 #pragma unroll
@@ -1265,7 +1272,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   }
   if (!done) stream_B_simt<T, G_T, VEC, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, apx, wring, wbar, rp, wpart);
   __syncthreads();
-  float* gpart = p.part + (((size_t)u * p.nA + q) * G) * ldp;
+  float* gpart = p.part + (((size_t)u * 2 * p.nA + pidx) * G) * ldp;
   for (int i = tid; i < G * ldp; i += kPT) {
     const int g = i / ldp, col = i % ldp;
     float mm = -CUDART_INF_F, ll = 0.f, aa = 0.f;
@@ -1280,7 +1287,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    sh.last = atomicAdd(&cu[1], 1u) == (unsigned)nparts - 1u;
+    sh.last = atomicAdd(&cu[1], 1u) == (unsigned)narrive - 1u;
     if (sh.last) __threadfence();
   }
   __syncthreads();
@@ -1329,7 +1336,7 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
   if (tid == 0) sh.next_ticket = atomicAdd(&p.ctrl[0], 1u);
   __syncthreads();
   RingPos rp(nsw);
-  const int per_slot = 2 * p.nA;  // A(u, 0..nA-1) then B(u - lag, 0..nA-1)
+  const int per_slot = 2 * p.nA;  // A(u, 0..nA-1) then B(u - lag, 0..nA-1); tail slots: half B items
   for (;;) {
     const unsigned t = sh.next_ticket;
     __syncthreads();
@@ -1344,13 +1351,14 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
     const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
     const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
     int kind = 0;
-    if (r < p.nA) {
-      if (slot < p.units)
-        kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, sbar, sphase, rp, sh);
-    } else {
-      const int u = slot - p.lag;
-      if (u >= 0 && u < p.units)
-        kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, u, r - p.nA, ring, wring, wbar, ents, rp, sh);
+    if (slot >= p.units) {  // tail slot: no A items left, all 2 nA tickets are half-size B items
+      kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
+                                      rp, sh);
+    } else if (r < p.nA) {
+      kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, sbar, sphase, rp, sh);
+    } else if (slot >= p.lag) {
+      kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
+                                      rp, sh);
     }
     fence_proxy_async();  // this item's generic shared-memory writes precede the next item's TMA writes
     __syncthreads();
