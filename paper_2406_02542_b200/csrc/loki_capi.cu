@@ -265,7 +265,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   const int e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   pl->G_T = G_T;
   // tensor-core phase 3 (bf16): 16-row stages of K and V (64 * D bytes)
-  const bool mma = g.dtype == LOKI_DTYPE_BF16 && env_int("LOKI_PIPE_MMA", 1) != 0;
+  const bool mma = g.dtype == LOKI_DTYPE_BF16;  // bf16 caches: tensor-core phase 3 (compiled in, not optional)
   const int stage = mma ? 32 * g.D : env_int("LOKI_PIPE_STAGE_KB", 4) * 1024;
   if (!tma_geom(a, G_T, &pl->tg, stage)) return fail(LOKI_ERR_UNSUPPORTED, "pipe: TMA geometry");
   loki::PipeParams& p = pl->p;
@@ -282,8 +282,12 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if (mma) p.r3 = 8;
   // one lane per lead row when the row is a TMA swizzle span (64 / 128 B) and r1 covers whole lanes
   const int lead_rb = p.dbox * e;
-  p.lead_swz = (G_T == 1 && (lead_rb == 64 || lead_rb == 128) && p.r1 % 64 == 0 && env_int("LOKI_LEAD_LPR", 1) != 0)
-                   ? lead_rb : 0;
+  // G == 1: one lane per lead row (r1 % 64); G >= 2 (bf16): tensor-core scores on 16-row blocks
+  const bool lead_ok = (lead_rb == 64 || lead_rb == 128) && env_int("LOKI_LEAD_LPR", 1) != 0 &&
+                       (G_T == 1 ? p.r1 % 64 == 0 : (g.dtype == LOKI_DTYPE_BF16 && p.r1 % 16 == 0));
+  p.lead_swz = lead_ok ? lead_rb : 0;
+  if (g.dtype == LOKI_DTYPE_BF16 && G_T >= 2 && p.lead_swz == 0)  // bf16 groups need the tensor-core lead path
+    return fail(LOKI_ERR_UNSUPPORTED, "pipe: bf16 query groups need 64 / 128 B lead rows (d = %d)", d);
   // chunk = part: kNB 128-row blocks per warp in the B-item row scan (loki_pipe.cu)
   const int kNB = G_T >= 4 ? 1 : 4 / G_T;
   const int Lc = kNB * 128 * loki::pipe_warps();

@@ -499,7 +499,7 @@ __device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t*
                                              uint32_t* hist, int HB, int hshift) {
   constexpr int E = sizeof(T);
   constexpr int RPW1 = 32 / LPR1;
-  constexpr int U = 4;  // independent rows in flight per lane
+  constexpr int U = G_T >= 4 ? 2 : 4;  // independent rows in flight per lane (register budget: 2 CTAs / SM)
   const int lane = lane_id();
   const int row_bytes = p.dbox * E;
   const int nch1 = p.dbox / VEC;
@@ -598,6 +598,53 @@ __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint
   }
 }
 
+// Phase-1 stage consumed by ONE warp on the tensor cores (bf16 caches, query
+// groups G >= 2: scores[rows x G] = K_lead[rows x dbox] . Q[dbox x G] is a real
+// contraction).  q is split into three bf16 terms (hi + mid + lo == the fp32
+// value), one mma n-tile each, so a lane sums its own three fragments: the
+// scores carry fp32-level error, inside the tie band of the selection parity
+// (SURVEY 8c O4).  Lead rows are RB = 64 / 128 B, TMA-swizzled.  Lane
+// (g8, t4) holds rows {g8, g8 + 8} x heads {2 t4, 2 t4 + 1} of each 16-row block.
+template <int RB, int G_T>
+__device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint8_t* tile, int rows_here,
+                                                 const uint32_t (&qf)[3][4][2], int G, uint32_t* keys0,
+                                                 float* approx0, uint32_t* hist, int HB, int hshift) {
+  constexpr int KS = RB / 32;  // k-steps of 16 bf16 columns
+  const int lane = lane_id();
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const uint32_t tb = smem_u32(tile);
+  const int rA = (lane & 7) | (((lane >> 3) & 1) << 3);
+  const int cA = (lane >> 4) & 1;
+  for (int b0 = 0; b0 < p.r1; b0 += 16) {
+    float S[3][4];
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) S[t][i] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int r = b0 + rA, c = 2 * ks + cA;
+      const int sw = RB == 64 ? ((r >> 1) & 3) : (r & 7);
+      uint32_t a[4];
+      ldsm_x4(tb + (uint32_t)(r * RB + ((c ^ sw) << 4)), a);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) mma_bf16(S[t], a, qf[t][ks][0], qf[t][ks][1]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = b0 + g8 + (i >> 1) * 8;
+      const int h = 2 * t4 + (i & 1);
+      if (h < G && rr < rows_here) {
+        const float sc = (S[0][i] + S[1][i]) + S[2][i];
+        const uint32_t key = order_key(sc);
+        keys0[(size_t)h * p.kstride + rr] = key;
+        if (approx0 != nullptr) approx0[(size_t)h * p.S_cap + rr] = sc;
+        atomicAdd(&hist[h * HB + (key >> hshift)], 1u);
+      }
+    }
+  }
+}
+
 template <typename T, int G_T, int VEC>
 __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, int c, uint8_t* ring,
                        uint8_t* wring, uint64_t* wbar, uint32_t* hist, uint64_t* sbar, unsigned& sphase, RingPos& rp,
@@ -643,7 +690,47 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
     uint32_t* keys_u = p.keys + (size_t)u * G * p.kstride + row0;
     float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap + row0 : nullptr;
     constexpr int E = sizeof(T);
-    if (G_T == 1 && p.lead_swz != 0) {  // one lane per row (swizzled lead rows)
+    bool consumed = false;
+    if constexpr (sizeof(T) == 2 && G_T >= 2) {
+      if (p.lead_swz != 0) {  // tensor-core scores for the query group
+        uint32_t qf[3][4][2];   // [part][k-step][reg]: B operand, k = 16 ks + 2 t4 + {0, 1, 8, 9}, n = head
+        const int g8 = lane >> 2, t4 = lane & 3;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          float v[4], r1v[4], r2v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int dim = 16 * ks + 2 * t4 + (i & 1) + (i >> 1) * 8;
+            v[i] = (g8 < G && dim < p.d) ? p.q_hat[(qrow0 + g8) * p.D + dim] : 0.f;
+            r1v[i] = v[i] - bf16_hi(v[i]);
+            r2v[i] = r1v[i] - bf16_hi(r1v[i]);
+          }
+          qf[0][ks][0] = pack_bf16(v[0], v[1]);
+          qf[0][ks][1] = pack_bf16(v[2], v[3]);
+          qf[1][ks][0] = pack_bf16(r1v[0], r1v[1]);
+          qf[1][ks][1] = pack_bf16(r1v[2], r1v[3]);
+          qf[2][ks][0] = pack_bf16(r2v[0], r2v[1]);
+          qf[2][ks][1] = pack_bf16(r2v[2], r2v[3]);
+        }
+        for (int k = 0; k < mine; ++k, rp.advance(1)) {
+          mbar_wait(&wbar[rp.slot], rp.phase);
+          const uint8_t* tile = wring + rp.slot * SB;
+          const int i = w + k * kPW;
+          const int rows_here = min(R1, n - i * R1);
+          uint32_t* k0 = keys_u + i * R1;
+          float* a0 = approx_u ? approx_u + i * R1 : nullptr;
+          if (p.lead_swz == 64)
+            lead_consume_mma<64, G_T>(p, tile, rows_here, qf, G, k0, a0, hist, HB, hshift);
+          else
+            lead_consume_mma<128, G_T>(p, tile, rows_here, qf, G, k0, a0, hist, HB, hshift);
+          __syncwarp();
+          if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+        }
+        consumed = true;
+      }
+    }
+    if (consumed || (sizeof(T) == 2 && G_T >= 2)) {  // (bf16 groups always take the tensor-core path: host)
+    } else if (G_T == 1 && p.lead_swz != 0) {  // one lane per row (swizzled lead rows)
       constexpr int Q2 = 32;  // element pairs of the widest lead row (128 B of bf16)
       unsigned long long q2[Q2];
 #pragma unroll
@@ -667,7 +754,7 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
         __syncwarp();
         if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
       }
-    } else
+    } else if constexpr (!(sizeof(T) == 2 && G_T >= 2))
     for (int k = 0; k < mine; ++k, rp.advance(1)) {
       mbar_wait(&wbar[rp.slot], rp.phase);
       const uint8_t* tile = wring + rp.slot * SB;
@@ -1263,14 +1350,10 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   const int ldp = D + 2;
   float* wpart = reinterpret_cast<float*>(ring);  // [kPW][G_T][D + 2]; every ring slot has been consumed
   const int row_base = (int)(((long long)b * p.Hkv + hk) * p.unit_rows);
-  bool done = false;
-  if constexpr (sizeof(T) == 2) {
-    if (p.mma) {
-      stream_B_mma<G_T, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, wring, wbar, rp, wpart);
-      done = true;
-    }
-  }
-  if (!done) stream_B_simt<T, G_T, VEC, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, apx, wring, wbar, rp, wpart);
+  if constexpr (sizeof(T) == 2)  // bf16: always the tensor-core phase 3 (host sets p.mma)
+    stream_B_mma<G_T, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, wring, wbar, rp, wpart);
+  else
+    stream_B_simt<T, G_T, VEC, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, apx, wring, wbar, rp, wpart);
   __syncthreads();
   float* gpart = p.part + (((size_t)u * 2 * p.nA + pidx) * G) * ldp;
   for (int i = tid; i < G * ldp; i += kPT) {
