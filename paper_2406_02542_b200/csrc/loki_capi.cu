@@ -304,7 +304,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if (occ < 1) return fail(LOKI_ERR_UNSUPPORTED, "pipe: kernel does not fit on an SM (%zu B smem)", pl->smem);
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
-  const double lagx = env_int("LOKI_PIPE_LAG_X10", 40) / 10.0;
+  // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn
+  const double lagx = env_int("LOKI_PIPE_LAG_X10", 40 * G) / 10.0;
   int lag = (int)ceil(lagx * pl->grid / (double)(2 * p.nA));
   p.lag = lag < 1 ? 1 : (lag > units ? units : lag);
   p.n_tickets = (long long)(units + p.lag) * (2 * p.nA);

@@ -1236,6 +1236,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
       }
     }
   }
+  if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();  // ready observed (trace: wait vs work)
   __syncthreads();
   const bool split = p.split_k != 0;
   const size_t qrow0 = (size_t)b * p.Hq + (size_t)hk * G;
@@ -1452,7 +1453,7 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
       tr[0] = t0;
       tr[1] = globaltimer();
       tr[2] = (long long)smid | ((long long)kind << 16) | ((long long)blockIdx.x << 32);
-      tr[3] = (kind >= 3) ? sh.t_sel : 0;
+      tr[3] = (kind >= 2) ? sh.t_sel : 0;
     }
   }
 }

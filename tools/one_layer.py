@@ -81,7 +81,11 @@ if os.environ.get("LOKI_TRACE") and call.plan()["ctas_per_unit"] == 0:
         m = kind == kd
         if m.any():
             print(f"  {nm:9s} n={m.sum():5d} median {np.median(dur[m]):7.2f} us  mean {dur[m].mean():7.2f}  max {dur[m].max():7.2f}  busy-share {dur[m].sum() / dur.sum() * 100:5.1f}%")
-    lastm = t[:, 3] != 0
+    bm = (kind == 2) & (t[:, 3] != 0)
+    if bm.any():
+        wait = (t[bm, 3] - t[bm, 0]) / 1e3
+        print(f"  B wait-for-ready: median {np.median(wait):6.2f} us  mean {wait.mean():6.2f}  max {wait.max():6.2f}")
+    lastm = (t[:, 3] != 0) & (kind >= 3)
     tail = (t[lastm, 1] - t[lastm, 3]) / 1e3
     for kd, nm in ((3, "select"), (4, "merge")):
         m = kind[lastm] == kd
