@@ -240,7 +240,7 @@ struct PipePlan {
   int grid = 0;
   size_t smem = 0;
   size_t ws = 0;
-  size_t off_hist = 0, off_keys = 0, off_tcs = 0, off_poff = 0, off_part = 0, off_logits = 0;
+  size_t off_hist = 0, off_keys = 0, off_tcs = 0, off_poff = 0, off_part = 0, off_spec = 0, off_logits = 0;
 };
 
 // The persistent pipelined kernel (loki_pipe.cu) serves the attending TOPK
@@ -295,6 +295,9 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   p.Lc = Lc;
   p.nA = loki::ceil_div(a->S_max, Lc);
   p.units = units;
+  // speculative boundary-bin candidates (ranking-free path only: idx_out needs per-part counts)
+  p.spec = env_int("LOKI_SPEC", 0) != 0 && G_T <= 4 && a->idx_out == nullptr;  // opt-in: r01 measured a net loss
+  p.ccap = a->S_max / 4 > 2048 ? a->S_max / 4 : 2048;
   pl->smem = loki::pipe_layout(G_T, &p);
   const size_t ring = (size_t)loki::pipe_warps() * p.nst * p.stage_bytes;
   if ((size_t)loki::pipe_warps() * G_T * (g.D + 2) * 4 > ring || p.cand_cap < 256)
@@ -323,6 +326,12 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if (a->idx_out != nullptr) off = loki::align_up(off + (size_t)units * G * 2 * p.nA * 4, 256);
   pl->off_part = off;
   off = loki::align_up(off + (size_t)units * 2 * p.nA * G * (g.D + 2) * 4, 256);  // full or half parts
+  pl->off_spec = off;
+  if (p.spec) {
+    off = loki::align_up(off + (size_t)units * G * p.ccap * 8, 256);  // cbuf
+    off = loki::align_up(off + (size_t)units * G * 4, 256);           // ccnt (zeroed, self-resetting)
+    off = loki::align_up(off + (size_t)units * G * p.nA * 4, 256);    // cwin
+  }
   pl->off_logits = off;
   if (a->weights_out != nullptr) off = loki::align_up(off + (size_t)units * G * g.S_cap * 4, 256);
   pl->ws = off;
@@ -358,6 +367,14 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   p.keys = reinterpret_cast<uint32_t*>(ws + pl.off_keys);
   p.tcs = reinterpret_cast<unsigned long long*>(ws + pl.off_tcs);
   p.poff = a->idx_out ? reinterpret_cast<uint32_t*>(ws + pl.off_poff) : nullptr;
+  if (p.spec) {
+    size_t o = pl.off_spec;
+    p.cbuf = reinterpret_cast<unsigned long long*>(ws + o);
+    o = loki::align_up(o + (size_t)p.units * p.G * p.ccap * 8, 256);
+    p.ccnt = reinterpret_cast<uint32_t*>(ws + o);
+    o = loki::align_up(o + (size_t)p.units * p.G * 4, 256);
+    p.cwin = reinterpret_cast<uint32_t*>(ws + o);
+  }
   p.part = reinterpret_cast<float*>(ws + pl.off_part);
   p.logits = a->weights_out ? reinterpret_cast<float*>(ws + pl.off_logits) : nullptr;
   p.debug = env_int("LOKI_DEBUG", 0);

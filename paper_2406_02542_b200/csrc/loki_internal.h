@@ -82,6 +82,11 @@ struct PipeParams {
   uint32_t* poff;    // [units][G][2 nA] idx_out offset of each half part (idx_out only)
   float* part;       // [units][2 nA][G][D + 2] per-part (acc[D], m, l); tail units use half parts
   float* logits;     // [units][G][S_cap] exact logits (weights_out only) or null
+  int spec;          // 1: A items publish boundary-bin candidates (selection skips the key scan)
+  int ccap;          // candidate capacity per (unit, head)
+  unsigned long long* cbuf;  // [units][G][ccap] candidate composites
+  uint32_t* ccnt;    // [units][G] candidate counts (zero between launches)
+  uint32_t* cwin;    // [units][G][nA] each chunk's bin window lo | hi << 16
   long long* trace;  // optional [n_tickets][4] {start, end, sm | kind << 16 | block << 32, tail start}
   int debug;
 };

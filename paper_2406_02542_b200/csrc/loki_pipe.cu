@@ -222,6 +222,7 @@ __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
 // flight while this one is scanned).  `sbar` are two mbarriers owned by the
 // selection; `sphase` holds their parity bits (identical in every thread).
 constexpr int kCK = 4096;  // keys per chunk (16 KB)
+constexpr int kSpecW = 2;  // speculative candidate window: boundary-bin estimate +- kSpecW bins
 
 struct KeyStream {
   const uint32_t* src;
@@ -299,13 +300,15 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
   unsigned long long* candC = candB + cap;
   const int Lh = p.Lc / 2;                      // idx_out offsets at half-part granularity
   const int nhp = ceil_div(S > 0 ? S : 1, Lh);
+  const int nparts_a = ceil_div(S > 0 ? S : 1, p.Lc);
   for (int g = 0; g < G; ++g) {
     const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
     uint32_t* gh = p.hist + ((size_t)u * G + g) * HB;
     uint32_t* poff = offsets ? p.poff + ((size_t)u * G + g) * 2 * p.nA : nullptr;  // per half part
     KeyStream ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
     if (g == 0) sel_stamp(p, u, 0);
-    if (kb > 0) ks.start();  // speculative: the compaction pass below almost always runs
+    const bool spec = p.spec && !offsets;
+    if (kb > 0 && !spec) ks.start();  // prefetch: the compaction pass below almost always runs
     for (int i = tid; i < HB; i += kPT) {
       hist[i] = __ldcg(&gh[i]);
       gh[i] = 0u;  // ready for the next launch
@@ -323,8 +326,46 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
     int nb = hb;
     unsigned need = (unsigned)kb - sh.fb_above, cnt = sh.fb_cnt;
     int ncand = 0;
-    bool listed = false, started = true;
-    for (;;) {
+    bool listed = false, started = !spec;
+    if (spec) {
+      const size_t ug = (size_t)u * G + g;
+      const unsigned total = __ldcg(&p.ccnt[ug]);
+      if (tid == 0) sh.ncand = (total <= (unsigned)p.ccap && cnt <= (unsigned)cap) ? 1 : 0;
+      __syncthreads();
+      for (int q = tid; q < nparts_a; q += kPT) {
+        const uint32_t wv = __ldcg(&p.cwin[ug * p.nA + q]);
+        if (P < (wv & 0xFFFFu) || P > (wv >> 16)) sh.ncand = 0;  // a chunk's window misses the boundary bin
+      }
+      __syncthreads();
+      const bool use = sh.ncand != 0;
+      __syncthreads();
+      if (tid == 0) {
+        sh.ncand = 0;
+        p.ccnt[ug] = 0u;  // ready for the next launch
+      }
+      __syncthreads();
+      if (use) {
+        const unsigned long long* cb = p.cbuf + ug * p.ccap;
+        for (int i0 = 0; i0 < (int)total; i0 += 4 * kPT) {
+          unsigned long long cv[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int i = i0 + x * kPT + tid;
+            cv[x] = i < (int)total ? __ldcg(&cb[i]) : 0ull;
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int i = i0 + x * kPT + tid;
+            append_if(i < (int)total && (cv[x] >> (64 - nb)) == P, cv[x], candA, &sh.ncand);
+          }
+        }
+        __syncthreads();
+        ncand = sh.ncand;
+        if (tid == 0) sh.ncand_first = ncand;
+        listed = (unsigned)ncand == cnt;  // always true when the windows cover the bin
+      }
+    }
+    for (; !listed;) {
       if (!started) ks.start();
       started = false;
       if (cnt <= (unsigned)cap) {  // compact the rows matching P (and count the rows above P per part)
@@ -495,8 +536,8 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
 // ------------------------------------------------------------------ item A
 template <typename T, int G_T, int VEC, int LPR1>
 __device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t* tile, int rows_here,
-                                             const float (&q1)[G_T][VEC], int G, uint32_t* keys0, float* approx0,
-                                             uint32_t* hist, int HB, int hshift) {
+                                             const float (&q1)[G_T][VEC], int G, uint32_t* keys0, uint32_t* kl,
+                                             float* approx0, uint32_t* hist, int HB, int hshift) {
   constexpr int E = sizeof(T);
   constexpr int RPW1 = 32 / LPR1;
   constexpr int U = G_T >= 4 ? 2 : 4;  // independent rows in flight per lane (register budget: 2 CTAs / SM)
@@ -533,6 +574,7 @@ __device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t*
           if (sl == 0 && rr < rows_here) {
             const uint32_t key = order_key(acc[u]);
             keys0[(size_t)g * p.kstride + rr] = key;
+            if (kl != nullptr) kl[g * p.Lc + rr] = key;
             if (approx0 != nullptr) approx0[(size_t)g * p.S_cap + rr] = acc[u];
             atomicAdd(&hist[g * HB + (key >> hshift)], 1u);
           }
@@ -559,7 +601,7 @@ __device__ __forceinline__ unsigned long long pk2(uint32_t lo, uint32_t hi) {
 template <typename T, int RB>
 __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint8_t* tile, int rows_here,
                                                  const unsigned long long (&q2)[32], uint32_t* keys0,
-                                                 float* approx0, uint32_t* hist, int hshift) {
+                                                 uint32_t* kl, float* approx0, uint32_t* hist, int hshift) {
   constexpr int NCH = RB / 16;
   const int lane = lane_id();
   for (int r0 = 0; r0 < p.r1; r0 += 64) {
@@ -591,6 +633,7 @@ __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint
       if (rr < rows_here) {
         const uint32_t key = order_key(sc);
         keys0[rr] = key;
+        if (kl != nullptr) kl[rr] = key;
         if (approx0 != nullptr) approx0[rr] = sc;
         atomicAdd(&hist[key >> hshift], 1u);
       }
@@ -608,7 +651,7 @@ __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint
 template <int RB, int G_T>
 __device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint8_t* tile, int rows_here,
                                                  const uint32_t (&qf)[3][4][2], int G, uint32_t* keys0,
-                                                 float* approx0, uint32_t* hist, int HB, int hshift) {
+                                                 uint32_t* kl, float* approx0, uint32_t* hist, int HB, int hshift) {
   constexpr int KS = RB / 32;  // k-steps of 16 bf16 columns
   const int lane = lane_id();
   const int g8 = lane >> 2, t4 = lane & 3;
@@ -638,6 +681,7 @@ __device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint
         const float sc = (S[0][i] + S[1][i]) + S[2][i];
         const uint32_t key = order_key(sc);
         keys0[(size_t)h * p.kstride + rr] = key;
+        if (kl != nullptr) kl[h * p.Lc + rr] = key;
         if (approx0 != nullptr) approx0[(size_t)h * p.S_cap + rr] = sc;
         atomicAdd(&hist[h * HB + (key >> hshift)], 1u);
       }
@@ -647,8 +691,8 @@ __device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint
 
 template <typename T, int G_T, int VEC>
 __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, int c, uint8_t* ring,
-                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, uint64_t* sbar, unsigned& sphase, RingPos& rp,
-                       PipeShared& sh) {
+                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, uint32_t* kloc, uint64_t* sbar,
+                       unsigned& sphase, RingPos& rp, PipeShared& sh) {
   constexpr int E = sizeof(T);
   const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int nsw = p.nst, SB = p.stage_bytes;
@@ -688,6 +732,8 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
         q1[g][v] = (g < G && col < p.d && sl < nch1) ? p.q_hat[(qrow0 + g) * p.D + col] : 0.f;
       }
     uint32_t* keys_u = p.keys + (size_t)u * G * p.kstride + row0;
+    // spec: the chunk's keys also stay in shared memory ([G][Lc], the idle B-item entry region)
+    auto kl0 = [&](int box) -> uint32_t* { return p.spec ? kloc + box * p.r1 : nullptr; };
     float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap + row0 : nullptr;
     constexpr int E = sizeof(T);
     bool consumed = false;
@@ -720,9 +766,9 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
           uint32_t* k0 = keys_u + i * R1;
           float* a0 = approx_u ? approx_u + i * R1 : nullptr;
           if (p.lead_swz == 64)
-            lead_consume_mma<64, G_T>(p, tile, rows_here, qf, G, k0, a0, hist, HB, hshift);
+            lead_consume_mma<64, G_T>(p, tile, rows_here, qf, G, k0, kl0(i), a0, hist, HB, hshift);
           else
-            lead_consume_mma<128, G_T>(p, tile, rows_here, qf, G, k0, a0, hist, HB, hshift);
+            lead_consume_mma<128, G_T>(p, tile, rows_here, qf, G, k0, kl0(i), a0, hist, HB, hshift);
           __syncwarp();
           if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
         }
@@ -748,9 +794,9 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
         uint32_t* k0 = keys_u + i * R1;
         float* a0 = approx_u ? approx_u + i * R1 : nullptr;
         if (p.lead_swz == 64)
-          lead_consume_lpr<T, 64>(p, tile, rows_here, q2, k0, a0, hist, hshift);
+          lead_consume_lpr<T, 64>(p, tile, rows_here, q2, k0, kl0(i), a0, hist, hshift);
         else
-          lead_consume_lpr<T, 128>(p, tile, rows_here, q2, k0, a0, hist, hshift);
+          lead_consume_lpr<T, 128>(p, tile, rows_here, q2, k0, kl0(i), a0, hist, hshift);
         __syncwarp();
         if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
       }
@@ -763,18 +809,47 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
       uint32_t* k0 = keys_u + i * R1;
       float* a0 = approx_u ? approx_u + i * R1 : nullptr;
       switch (LPR1) {
-        case 1: lead_consume<T, G_T, VEC, 1>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
-        case 2: lead_consume<T, G_T, VEC, 2>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
-        case 4: lead_consume<T, G_T, VEC, 4>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
-        case 8: lead_consume<T, G_T, VEC, 8>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
-        case 16: lead_consume<T, G_T, VEC, 16>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
-        default: lead_consume<T, G_T, VEC, 32>(p, tile, rows_here, q1, G, k0, a0, hist, HB, hshift); break;
+        case 1: lead_consume<T, G_T, VEC, 1>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
+        case 2: lead_consume<T, G_T, VEC, 2>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
+        case 4: lead_consume<T, G_T, VEC, 4>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
+        case 8: lead_consume<T, G_T, VEC, 8>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
+        case 16: lead_consume<T, G_T, VEC, 16>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
+        default: lead_consume<T, G_T, VEC, 32>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
       }
       __syncwarp();  // every lane is done with the slot before it is refilled
       if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
     }
   }
   __syncthreads();
+  if (p.spec && n > 0) {
+    // Speculative candidates (SURVEY 8(a) R7 made cheap): this chunk is a sample of the unit, so the
+    // unit's boundary bin is near the chunk's own k * n / S quantile.  Rows within kSpecW bins of
+    // it go to a per-(unit, head) list; the selection uses the list when every chunk's window holds
+    // the true boundary bin and falls back to scanning all keys otherwise.
+    const int kb = k_of(p, S);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int g = 0; g < G; ++g) {
+      int kq = (int)(((long long)kb * n + S / 2) / S);
+      kq = kq < 1 ? 1 : (kq > n ? n : kq);
+      find_bin(hist + g * HB, HB, (unsigned)kq, sh);
+      const int lo = max(0, sh.fb_bin - kSpecW), hi = min(HB - 1, sh.fb_bin + kSpecW);
+      const size_t ug = (size_t)u * G + g;
+      if (tid == 0) p.cwin[ug * p.nA + c] = (uint32_t)lo | ((uint32_t)hi << 16);
+      unsigned long long* cb = p.cbuf + ug * p.ccap;
+      for (int j0 = 0; j0 < n; j0 += kPT) {
+        const int j = j0 + tid;
+        const uint32_t key = j < n ? kloc[g * p.Lc + j] : 0u;
+        const int bin = (int)(key >> hshift);
+        const bool m = j < n && bin >= lo && bin <= hi;
+        const unsigned bal = __ballot_sync(0xffffffffu, m);
+        unsigned base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&p.ccnt[ug], (unsigned)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned at = base + __popc(bal & lt);
+        if (m && at < (unsigned)p.ccap) cb[at] = comp_key(key, row0 + j);
+      }
+    }
+  }
   uint32_t* gh = p.hist + (size_t)u * G * HB;
   for (int i = tid; i < G * HB; i += kPT) {
     const uint32_t v = hist[i];
@@ -1439,7 +1514,7 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
       kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
                                       rp, sh);
     } else if (r < p.nA) {
-      kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, sbar, sphase, rp, sh);
+      kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, sbar, sphase, rp, sh);
     } else if (slot >= p.lag) {
       kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
                                       rp, sh);
@@ -1474,7 +1549,9 @@ size_t pipe_layout(int G_T, PipeParams* p) {
   const int hb = p->hbits > 8 ? p->hbits : 8;
   off = align_up(off + (size_t)G_T * (1u << hb) * 4, 16);
   p->off_ents = (int)off;
-  off = align_up(off + (size_t)p->Lc * 4 * (1 + (p->split_k ? G_T : 0)), 128);
+  const size_t ents_words = (size_t)p->Lc * (1 + (p->split_k ? G_T : 0));
+  const size_t spec_words = p->spec ? (size_t)p->Lc * G_T : 0;
+  off = align_up(off + 4 * (ents_words > spec_words ? ents_words : spec_words), 128);
   off += 1024;  // slack for aligning the dynamic shared memory base to 1024 B
   // ring during a selection: two key chunks of kCK keys, then three u64 candidate buffers
   const long long rest = (long long)kPW * p->nst * p->stage_bytes - 2LL * kCK * 4;
