@@ -104,7 +104,12 @@ loki_status loki_device_check(int32_t device);
  * + weighted-sum chain kernels.py:244-279 / linalg.py:76-92). */
 loki_status loki_decode(const loki_decode_args* args, void* stream);
 
-/* Scratch bytes loki_decode needs for `args` (0 for on-chip plans). */
+/* Scratch bytes loki_decode needs for `args` (0 for on-chip plans).
+ * The workspace must be ZERO-FILLED before its first use (cudaMemset); every
+ * launch leaves it zero-filled again (the persistent kernel's ticket counter,
+ * per-unit arrival counters and histograms reset themselves), so one
+ * workspace serves any number of launches on one stream.  Do not share one
+ * workspace between launches that may run concurrently. */
 loki_status loki_decode_workspace_bytes(const loki_decode_args* args, size_t* bytes);
 
 /* Launch plan chosen for `args`: CTAs per unit, rows per CTA, dynamic smem. */
