@@ -237,6 +237,7 @@ struct PipePlan {
   loki::PipeParams p{};
   TmaGeom tg{};
   int G_T = 1;
+  bool big = false;
   int grid = 0;
   size_t smem = 0;
   size_t ws = 0;
@@ -289,7 +290,11 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if (g.dtype == LOKI_DTYPE_BF16 && G_T >= 2 && p.lead_swz == 0)  // bf16 groups need the tensor-core lead path
     return fail(LOKI_ERR_UNSUPPORTED, "pipe: bf16 query groups need 64 / 128 B lead rows (d = %d)", d);
   // chunk = part: kNB 128-row blocks per warp in the B-item row scan (loki_pipe.cu)
-  const int kNB = G_T >= 4 ? 1 : 4 / G_T;
+  // MHA at long sequences: 2x larger chunks (fewer per-item latency bubbles; r01: TGT 683 -> 658 us,
+  // C2 213 -> 219 us, so only from 16K rows on)
+  pl->big = G_T == 1 && env_int("LOKI_PIPE_BIG", a->S_max >= 16384 ? 1 : 0) != 0;
+  const int nbg = pl->big ? 2 * loki::pipe_nb() : loki::pipe_nb();
+  const int kNB = G_T >= nbg ? 1 : nbg / G_T;
   const int Lc = kNB * 128 * loki::pipe_warps();
   if (Lc % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", Lc, p.r1);
   p.Lc = Lc;
@@ -303,7 +308,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if ((size_t)loki::pipe_warps() * G_T * (g.D + 2) * 4 > ring || p.cand_cap < 256)
     return fail(LOKI_ERR_UNSUPPORTED, "pipe: ring of %zu bytes too small", ring);
   if (pl->smem > kSmemMax) return fail(LOKI_ERR_UNSUPPORTED, "pipe: shared memory plan %zu bytes", pl->smem);
-  const int occ = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem);
+  const int occ = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem, pl->big);
   if (occ < 1) return fail(LOKI_ERR_UNSUPPORTED, "pipe: kernel does not fit on an SM (%zu B smem)", pl->smem);
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
@@ -383,7 +388,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   loki::TmaDesc maps[3];
   if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, p.mma != 0, p.lead_swz, maps))
     return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
-  cudaError_t e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream));
+  cudaError_t e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big);
   if (e == cudaSuccess) e = cudaGetLastError();
   return cuda_status(e, "loki_decode (pipe) launch");
 }

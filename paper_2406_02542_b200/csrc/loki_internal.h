@@ -150,9 +150,11 @@ bool pipe_supported(int dtype, int D, int G_T);
 // lead boxes {dbox, r1} (64 B promotion), K row gathers of columns [kcol0, D), V row gathers
 bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, int r1, int kcol0, bool mma,
                      int lead_swz, TmaDesc* maps);
+// big: 2x larger chunks (compiled for G == 1 only; long sequences amortise per-item latency)
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
-                        cudaStream_t st);
-int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem);
+                        cudaStream_t st, bool big);
+int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big);
 int pipe_warps();
+int pipe_nb();
 
 }  // namespace loki

@@ -44,6 +44,9 @@ using namespace tma;
 using fused::kMaxG;
 using fused::merge_state;
 
+#ifndef LOKI_PIPE_NB
+#define LOKI_PIPE_NB 4  // 128-row blocks per warp in a G = 1 chunk (Lc = NB * 128 * warps)
+#endif
 #ifndef LOKI_PIPE_WARPS
 #define LOKI_PIPE_WARPS 8
 #endif
@@ -1278,7 +1281,7 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
 }
 
 // B(u, q): rows [q * Lc, (q + 1) * Lc).  kNB 128-row blocks per warp.
-template <typename T, int G_T, int VEC, int D_T>
+template <typename T, int G_T, int VEC, int D_T, bool BIG>
 __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u, int q,
                       int half, uint8_t* ring, uint8_t* wring, uint64_t* wbar, uint32_t* ents, RingPos& rp,
                       PipeShared& sh) {
@@ -1286,7 +1289,8 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   constexpr int LPR3 = D_T / VEC;  // lanes per V row
   constexpr int RPW3 = 32 / LPR3;
   constexpr int ROWB = D_T * E;
-  constexpr int kNB = G_T >= 4 ? 1 : 4 / G_T;  // Lc == kNB * 128 * kPW (host)
+  constexpr int NBG = BIG ? 2 * LOKI_PIPE_NB : LOKI_PIPE_NB;  // 128-row blocks per warp at G = 1
+  constexpr int kNB = G_T >= NBG ? 1 : NBG / G_T;  // Lc == kNB * 128 * kPW (host)
   const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int nsw = p.nst, SB = p.stage_bytes;
   const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G, D = D_T;
@@ -1459,7 +1463,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
 }
 
 // ------------------------------------------------------------------ kernel
-template <typename T, int G_T, int VEC, int D_T>
+template <typename T, int G_T, int VEC, int D_T, bool BIG>
 __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
                                                           const __grid_constant__ CUtensorMap lead_map,
                                                           const __grid_constant__ CUtensorMap krow_map,
@@ -1511,12 +1515,12 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
     const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
     int kind = 0;
     if (slot >= p.units) {  // tail slot: no A items left, all 2 nA tickets are half-size B items
-      kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
+      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
                                       rp, sh);
     } else if (r < p.nA) {
       kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, sbar, sphase, rp, sh);
     } else if (slot >= p.lag) {
-      kind = item_B<T, G_T, VEC, D_T>(p, &krow_map, &vrow_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
+      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
                                       rp, sh);
     }
     fence_proxy_async();  // this item's generic shared-memory writes precede the next item's TMA writes
@@ -1538,6 +1542,7 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
 // ---------------------------------------------------------------- host side
 
 int pipe_warps() { return kPW; }
+int pipe_nb() { return LOKI_PIPE_NB; }
 
 size_t pipe_layout(int G_T, PipeParams* p) {
   size_t off = 0;
@@ -1559,9 +1564,9 @@ size_t pipe_layout(int G_T, PipeParams* p) {
   return off;
 }
 
-template <typename T, int G_T, int VEC, int D_T>
+template <typename T, int G_T, int VEC, int D_T, bool BIG>
 static cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st) {
-  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T>;
+  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG>;
   static size_t smem_set = 0;
   if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1582,9 +1587,9 @@ static cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, con
   return cudaLaunchKernelEx(&cfg, kern, p, m[0], m[1], m[2]);
 }
 
-template <typename T, int G_T, int VEC, int D_T>
+template <typename T, int G_T, int VEC, int D_T, bool BIG>
 static int occupancy_t(size_t smem) {
-  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T>;
+  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kPT, smem) != cudaSuccess) return 0;
@@ -1629,16 +1634,18 @@ bool pipe_supported(int dtype, int D, int G_T) {
   return (D == 64 || D == 128) && G_T <= 8;
 }
 
-int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem) {
-#define LOKI_OCC(T, GT, VEC, DT) occupancy_t<T, GT, VEC, DT>(smem)
+int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big) {
+#define LOKI_OCC(T, GT, VEC, DT) (big ? occupancy_t<T, GT, VEC, DT, GT == 1>(smem) : occupancy_t<T, GT, VEC, DT, false>(smem))
   LOKI_PIPE_DISPATCH(dtype, D, G_T, LOKI_OCC);
 #undef LOKI_OCC
   return 0;
 }
 
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
-                        cudaStream_t st) {
-#define LOKI_LAUNCH(T, GT, VEC, DT) launch_pipe_t<T, GT, VEC, DT>(p, grid, smem, maps, st)
+                        cudaStream_t st, bool big) {
+#define LOKI_LAUNCH(T, GT, VEC, DT)                                                   \
+  (big ? launch_pipe_t<T, GT, VEC, DT, GT == 1>(p, grid, smem, maps, st)              \
+       : launch_pipe_t<T, GT, VEC, DT, false>(p, grid, smem, maps, st))
   LOKI_PIPE_DISPATCH(dtype, p.D, G_T, LOKI_LAUNCH);
 #undef LOKI_LAUNCH
   return cudaErrorInvalidValue;

@@ -214,6 +214,8 @@ CASES = [  # B, Hq, Hkv, D, S, k_f, d_f, dtype
     (1, 2, 1, 96, 999, 0.25, 0.25, "f32"),
     (2, 2, 2, 128, 33, 0.5, 0.25, "bf16"),
     (4, 4, 1, 128, 2048, 0.25, 0.25, "bf16"),
+    (2, 2, 2, 128, 32768, 0.25, 0.25, "bf16"),  # long-sequence MHA: 8192-row pipe chunks
+    (1, 2, 2, 128, 20000, 0.25, 0.25, "bf16"),  # ... with a partial last chunk
 ]
 
 
