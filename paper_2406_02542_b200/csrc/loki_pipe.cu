@@ -1,1545 +1,21 @@
-// Persistent, dynamically scheduled Loki decode attention -- the TOPK hot
-// path on sm_100a (attention.py:166-185 loki_rank_and_attend, batched).
-//
-// Why not one cluster per (batch, KV head) unit (loki_decode_tma.cu): there
-// every resident CTA runs phase 1 -> selection -> phase 3 -> merge in
-// lockstep, so HBM idles while the whole GPU selects (profiles/r01_summary.md:
-// 53 % of the roofline).  Here a grid of resident CTAs draws tickets from one
-// global counter and each ticket is a work item:
-//
-//   A(u, c)  phase 1 over chunk c of unit u: TMA boxes of the leading d
-//            columns (L2 promotion 64 B: exactly d*S*e DRAM bytes), approx
-//            scores (kernels.py:223-241) -> order keys in an L2-resident
-//            workspace + a (1 << hbits)-bin histogram of their top bits.  The
-//            LAST A arriver of the unit runs the unit's top-k selection
-//            (linalg.py:95-118) and publishes the ascending union list.
-//   B(u, q)  phase 3 over part q of that list: tile::gather4 of the selected
-//            K and V rows, exact logits / sqrt(D), online softmax and V
-//            accumulation (kernels.py:244-279, linalg.py:76-92) -> a partial
-//            (m, l, acc) state.  The LAST B arriver merges the parts in fixed
-//            order and writes the output row.
-//
-// B tickets of unit u are issued `lag` units after its A tickets, so while
-// one CTA selects, the others keep streaming.  Items are 256 KB - 1 MB of HBM
-// traffic, so the tail of the grid is short and there is no wave
-// quantisation.  Everything is deterministic: selections are exact, partial
-// states are merged in fixed order (warps, then parts).
-//
-// Selection on 64-bit composite keys (order_key(score) << 32 | ~row): all
-// composites are distinct and "the k largest composites" is exactly the
-// reference's rule -- every score above the threshold, then threshold ties
-// lowest row first.  MSB radix select: the first digit comes from the
-// histogram built during phase 1; further digits are resolved over the
-// candidates (compacted to shared memory once they fit).
-#include <cuda.h>
-
-#include "loki_fused.cuh"
-#include "loki_tma.cuh"
+// Persistent pipelined Loki decode: host side (layout, dispatch).  The kernel
+// itself lives in loki_pipe_impl.cuh; its instantiations are split across the
+// loki_pipe_inst_*.cu translation units.
+#include "loki_pipe_impl.cuh"
 
 namespace loki {
 
-namespace {
+cudaError_t pipe_launch_bf16_64(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
+int pipe_occ_bf16_64(int, size_t, bool);
+cudaError_t pipe_launch_bf16_128(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
+int pipe_occ_bf16_128(int, size_t, bool);
+cudaError_t pipe_launch_bf16_256(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
+int pipe_occ_bf16_256(int, size_t, bool);
+cudaError_t pipe_launch_f32_64(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
+int pipe_occ_f32_64(int, size_t, bool);
+cudaError_t pipe_launch_f32_128(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
+int pipe_occ_f32_128(int, size_t, bool);
 
-using namespace tma;
-using fused::kMaxG;
-using fused::merge_state;
-
-#ifndef LOKI_PIPE_NB
-#define LOKI_PIPE_NB 4  // 128-row blocks per warp in a G = 1 chunk (Lc = NB * 128 * warps)
-#endif
-#ifndef LOKI_PIPE_WARPS
-#define LOKI_PIPE_WARPS 8
-#endif
-constexpr int kPW = LOKI_PIPE_WARPS;  // warps per CTA; every warp streams through its own TMA ring
-constexpr int kPT = kPW * 32;
-
-struct PipeShared {
-  unsigned next_ticket;
-  int last;
-  long long t_sel;
-  int fb_bin;
-  unsigned fb_above, fb_cnt;
-  int scan[kPW];
-  int ncand, ncand_first;
-  unsigned long long tsel;
-  unsigned long long Tc[kMaxG];
-  int wcnt[kPW][kMaxG + 1];
-  float gm[kMaxG], gl[kMaxG];
-};
-
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// generic-proxy shared-memory writes ordered before later TMA (async-proxy) writes
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__device__ __forceinline__ unsigned long long comp_key(uint32_t key, int j) {
-  return ((unsigned long long)key << 32) | (unsigned long long)(~(uint32_t)j);
-}
-
-// ---- tensor-core helpers (phase 3 on bf16 caches)
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
-}
-// d += a (16x16 bf16, row) * b (16x8 bf16, col), fp32 accumulate
-__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-      "{%0, %1, %2, %3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-// {lo -> bits 0..15, hi -> bits 16..31}, round to nearest even
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  return r;
-}
-// x = hi + lo with hi, lo bf16 (relative error of hi + lo ~ 2^-17)
-__device__ __forceinline__ float bf16_hi(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
-__device__ __forceinline__ float bf16_lo(float x) { return x - bf16_hi(x); }
-// 16 B chunk c of row r inside a 128B-swizzled block of 128 B rows (TMA SWIZZLE_128B)
-__device__ __forceinline__ uint32_t swz128(uint32_t base, int r, int c) {
-  return base + (uint32_t)(r * 128) + (uint32_t)(((c ^ (r & 7)) << 4));
-}
-
-__device__ __forceinline__ int k_of(const PipeParams& p, int S) {
-  if (S <= 0) return 0;
-  return p.k_fixed > 0 ? (p.k_fixed < S ? p.k_fixed : S) : resolve_fraction(p.k_f, S);
-}
-
-// Block-wide inclusive scan of one value per thread, in thread order.
-__device__ __forceinline__ unsigned block_incl_scan(unsigned v, PipeShared& sh, unsigned* total) {
-  const int lane = lane_id(), w = warp_id();
-  unsigned x = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const unsigned t = __shfl_up_sync(0xffffffffu, x, off);
-    if (lane >= off) x += t;
-  }
-  if (lane == 31) sh.scan[w] = (int)x;
-  __syncthreads();
-  unsigned before = 0, tot = 0;
-#pragma unroll
-  for (int i = 0; i < kPW; ++i) {
-    const unsigned c = (unsigned)sh.scan[i];
-    before += i < w ? c : 0u;
-    tot += c;
-  }
-  __syncthreads();
-  *total = tot;
-  return before + x;
-}
-
-// The bin holding the need-th largest element: largest b with
-// sum_{i>b} h[i] < need <= sum_{i>=b} h[i] -> sh.fb_bin / fb_above / fb_cnt.
-__device__ void find_bin(const uint32_t* h, int nbins, unsigned need, PipeShared& sh) {
-  const int tid = threadIdx.x;
-  const int per = nbins > kPT ? nbins / kPT : 1;  // nbins is a power of two
-  const int hi = nbins - tid * per;                // this thread owns bins [hi - per, hi)
-  unsigned s = 0;
-  if (hi > 0)
-    for (int i = 0; i < per; ++i) s += h[hi - 1 - i];
-  unsigned tot;
-  const unsigned incl = block_incl_scan(s, sh, &tot);
-  const unsigned excl = incl - s;
-  if (hi > 0 && excl < need && need <= incl) {
-    unsigned acc = excl;
-    for (int i = 0; i < per; ++i) {
-      const int b = hi - 1 - i;
-      if (acc + h[b] >= need) {
-        sh.fb_bin = b;
-        sh.fb_above = acc;
-        sh.fb_cnt = h[b];
-        break;
-      }
-      acc += h[b];
-    }
-  }
-  __syncthreads();
-}
-
-// Warp-aggregated append of `c` to dst when `m` (order within dst is irrelevant).
-__device__ __forceinline__ void append_if(bool m, unsigned long long c, unsigned long long* dst, int* counter) {
-  const int lane = lane_id();
-  const unsigned bal = __ballot_sync(0xffffffffu, m);
-  int base = 0;
-  if (lane == 0 && bal) base = atomicAdd(counter, __popc(bal));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (m) dst[base + __popc(bal & ((1u << lane) - 1u))] = c;
-}
-
-// ------------------------------------------------------------------ selection
-// Scans over a unit's keys are latency-bound L2 reads: every lane keeps
-// kSU uint4 loads (16 rows) in flight.  Warp w owns the contiguous rows
-// [ra, rb) (128-row aligned) so the emission can be ordered.
-constexpr int kSU = 4;
-
-__device__ __forceinline__ uint4 ld_keys4(const uint32_t* k, int j) {
-  return __ldcg(reinterpret_cast<const uint4*>(k + j));
-}
-__device__ __forceinline__ uint32_t u4_at(const uint4& v, int e) {
-  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
-}
-
-// f(jb, kk): lane's rows jb..jb+3 (caller masks rows >= rb); warp-uniform calls.
-template <typename F>
-__device__ __forceinline__ void scan_rows(const uint32_t* keys, int ra, int rb, F&& f) {
-  const int lane = lane_id();
-  for (int j0 = ra; j0 < rb; j0 += 128 * kSU) {
-    uint4 kk[kSU];
-#pragma unroll
-    for (int u = 0; u < kSU; ++u) {
-      const int jb = j0 + 128 * u + 4 * lane;
-      kk[u] = jb < rb ? ld_keys4(keys, jb) : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int u = 0; u < kSU; ++u) f(j0 + 128 * u + 4 * lane, kk[u]);
-  }
-}
-
-__device__ __forceinline__ int warp_excl_scan(int v, int* total) {
-  const int lane = lane_id();
-  int x = v;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, x, off);
-    if (lane >= off) x += t;
-  }
-  *total = __shfl_sync(0xffffffffu, x, 31);
-  return x - v;
-}
-
-// Keys of one head streamed through shared memory: two buffers of kCK keys
-// filled by cp.async.bulk (one L2 round trip per chunk, the next chunk in
-// flight while this one is scanned).  `sbar` are two mbarriers owned by the
-// selection; `sphase` holds their parity bits (identical in every thread).
-constexpr int kCK = 4096;  // keys per chunk (16 KB)
-constexpr int kSpecW = 2;  // speculative candidate window: boundary-bin estimate +- kSpecW bins
-
-struct KeyStream {
-  const uint32_t* src;
-  int S, kstride;
-  uint32_t* buf;  // [2][kCK]
-  uint64_t* sbar;
-  unsigned* sphase;
-  int nchunk;
-  __device__ void issue(int c) const {
-    if (threadIdx.x == 0 && c < nchunk) {
-      const int base = c * kCK;
-      int rows = min(kCK, kstride - base);
-      const unsigned bytes = (unsigned)(((rows * 4) + 15) & ~15);
-      uint64_t* bar = &sbar[c & 1];
-      mbar_expect_tx(bar, bytes);
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(buf + (c & 1) * kCK)),
-          "l"(src + base), "r"(bytes), "r"(smem_u32(bar))
-          : "memory");
-    }
-  }
-  // chunks 0 and 1 in flight (call once per pass, before run)
-  __device__ void start() const {
-    if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // keys were stored by generic st
-    issue(0);
-    issue(1);
-  }
-  // wait for the chunks start() issued without reading them
-  __device__ void drain() const {
-    for (int c = 0; c < 2 && c < nchunk; ++c) {
-      mbar_wait(&sbar[c], (*sphase >> c) & 1u);
-      *sphase ^= 1u << c;
-    }
-    __syncthreads();
-  }
-  // f(j0, keys, n): rows [j0, j0 + n) of the chunk in shared memory; every thread calls
-  template <typename F>
-  __device__ void run(F&& f) const {
-    for (int c = 0; c < nchunk; ++c) {
-      const int bi = c & 1;
-      mbar_wait(&sbar[bi], (*sphase >> bi) & 1u);
-      *sphase ^= 1u << bi;
-      f(c * kCK, buf + bi * kCK, min(kCK, S - c * kCK));
-      __syncthreads();  // every thread is done with buffer bi before it is refilled
-      issue(c + 2);
-    }
-  }
-};
-
-// LOKI_DEBUG & 16 (tuning only): %globaltimer at selection checkpoints, [units][8] at trace + 2^21
-__device__ __forceinline__ void sel_stamp(const PipeParams& p, int u, int k) {
-  if ((p.debug & 16) && p.trace != nullptr && threadIdx.x == 0) p.trace[(1 << 21) + (size_t)u * 8 + k] = globaltimer();
-}
-
-// Threshold of each head's top-k in unit u on 64-bit composite keys: the
-// last A arriver reads the level-0 histogram, compacts the boundary-bin rows
-// into shared memory with one pass over the keys (further histogram levels
-// only if they do not fit), narrows them (radix passes, then a direct rank
-// once <= 256 remain) and publishes tcs[u][g].  With idx_out it also
-// publishes each part's output offset (rows above the boundary per part +
-// candidates kept).
-template <int G_T>
-__device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, uint32_t* hist, uint64_t* sbar,
-                            unsigned& sphase, PipeShared& sh) {
-  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
-  const int G = p.G, hb = p.hbits, HB = 1 << hb;
-  uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
-  const int kb = k_of(p, S);
-  const int cap = p.cand_cap;
-  const bool offsets = p.idx_out != nullptr;
-  uint32_t* kbuf = reinterpret_cast<uint32_t*>(ring);
-  unsigned long long* candA = reinterpret_cast<unsigned long long*>(ring + 2 * kCK * 4);
-  unsigned long long* candB = candA + cap;
-  unsigned long long* candC = candB + cap;
-  const int Lh = p.Lc / 2;                      // idx_out offsets at half-part granularity
-  const int nhp = ceil_div(S > 0 ? S : 1, Lh);
-  const int nparts_a = ceil_div(S > 0 ? S : 1, p.Lc);
-  for (int g = 0; g < G; ++g) {
-    const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
-    uint32_t* gh = p.hist + ((size_t)u * G + g) * HB;
-    uint32_t* poff = offsets ? p.poff + ((size_t)u * G + g) * 2 * p.nA : nullptr;  // per half part
-    KeyStream ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
-    if (g == 0) sel_stamp(p, u, 0);
-    const bool spec = p.spec && !offsets;
-    if (kb > 0 && !spec) ks.start();  // prefetch: the compaction pass below almost always runs
-    for (int i = tid; i < HB; i += kPT) {
-      hist[i] = __ldcg(&gh[i]);
-      gh[i] = 0u;  // ready for the next launch
-    }
-    if (offsets)
-      for (int q = tid; q < nhp; q += kPT) poff[q] = 0u;
-    __syncthreads();
-    if (kb == 0) {
-      if (tid == 0) p.tcs[(size_t)u * G + g] = ~0ull;
-      continue;
-    }
-    find_bin(hist, HB, (unsigned)kb, sh);
-    if (g == 0) sel_stamp(p, u, 1);
-    unsigned long long P = (unsigned long long)sh.fb_bin;
-    int nb = hb;
-    unsigned need = (unsigned)kb - sh.fb_above, cnt = sh.fb_cnt;
-    int ncand = 0;
-    bool listed = false, started = !spec;
-    if (spec) {
-      const size_t ug = (size_t)u * G + g;
-      const unsigned total = __ldcg(&p.ccnt[ug]);
-      if (tid == 0) sh.ncand = (total <= (unsigned)p.ccap && cnt <= (unsigned)cap) ? 1 : 0;
-      __syncthreads();
-      for (int q = tid; q < nparts_a; q += kPT) {
-        const uint32_t wv = __ldcg(&p.cwin[ug * p.nA + q]);
-        if (P < (wv & 0xFFFFu) || P > (wv >> 16)) sh.ncand = 0;  // a chunk's window misses the boundary bin
-      }
-      __syncthreads();
-      const bool use = sh.ncand != 0;
-      __syncthreads();
-      if (tid == 0) {
-        sh.ncand = 0;
-        p.ccnt[ug] = 0u;  // ready for the next launch
-      }
-      __syncthreads();
-      if (use) {
-        const unsigned long long* cb = p.cbuf + ug * p.ccap;
-        for (int i0 = 0; i0 < (int)total; i0 += 4 * kPT) {
-          unsigned long long cv[4];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const int i = i0 + x * kPT + tid;
-            cv[x] = i < (int)total ? __ldcg(&cb[i]) : 0ull;
-          }
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const int i = i0 + x * kPT + tid;
-            append_if(i < (int)total && (cv[x] >> (64 - nb)) == P, cv[x], candA, &sh.ncand);
-          }
-        }
-        __syncthreads();
-        ncand = sh.ncand;
-        if (tid == 0) sh.ncand_first = ncand;
-        listed = (unsigned)ncand == cnt;  // always true when the windows cover the bin
-      }
-    }
-    for (; !listed;) {
-      if (!started) ks.start();
-      started = false;
-      if (cnt <= (unsigned)cap) {  // compact the rows matching P (and count the rows above P per part)
-        if (tid == 0) sh.ncand = 0;
-        __syncthreads();
-        const unsigned long long Pc = P;
-        const int sh64 = 64 - nb;
-        ks.run([&](int j0, const uint32_t* kc, int nrow) {
-          for (int i0 = 0; i0 < nrow; i0 += 4 * kPT) {
-            const int il = i0 + 4 * tid;
-            const uint4 kk = *reinterpret_cast<const uint4*>(kc + il);
-            int above = 0;
-            bool any = false;
-            if (nb <= 32) {  // prefix inside the 32-bit key: cheap tests, composites only for candidates
-              const int s32 = 32 - nb;
-              const uint32_t P32 = (uint32_t)Pc;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const bool ok = il + e < nrow;
-                const uint32_t pre = u4_at(kk, e) >> s32;
-                above += (ok && pre > P32) ? 1 : 0;
-                any |= ok && pre == P32;
-              }
-            } else {
-              any = true;
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                above += (il + e < nrow && (comp_key(u4_at(kk, e), j0 + il + e) >> sh64) > Pc) ? 1 : 0;
-            }
-            if (__any_sync(0xffffffffu, any)) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const unsigned long long c = comp_key(u4_at(kk, e), j0 + il + e);
-                append_if(il + e < nrow && (c >> sh64) == Pc, c, candA, &sh.ncand);
-              }
-            }
-            if (offsets) {  // a warp's 128 rows lie inside one half part (Lc / 2 % 128 == 0)
-              above = __reduce_add_sync(0xffffffffu, above);
-              const int jw = j0 + i0 + 128 * w;
-              if (lane == 0 && above) atomicAdd(&poff[jw / Lh], (uint32_t)above);
-            }
-          }
-        });
-        ncand = sh.ncand;
-        if (tid == 0) sh.ncand_first = ncand;
-        listed = true;
-        break;
-      }
-      if (cnt == need) {  // exact boundary bin, too large to list: drain the prefetched chunks
-        ks.drain();
-        break;
-      }
-      // one more histogram level over every row matching P
-      const int bits = min(hb, 64 - nb);
-      for (int i = tid; i < (1 << bits); i += kPT) hist[i] = 0u;
-      __syncthreads();
-      const unsigned long long Pc = P;
-      const int sh64 = 64 - nb;
-      ks.run([&](int j0, const uint32_t* kc, int nrow) {
-        for (int i = tid; i < nrow; i += kPT) {
-          const unsigned long long c = comp_key(kc[i], j0 + i);
-          if ((c >> sh64) == Pc) atomicAdd(&hist[(c >> (sh64 - bits)) & ((1ull << bits) - 1)], 1u);
-        }
-      });
-      find_bin(hist, 1 << bits, need, sh);
-      P = (P << bits) | (unsigned long long)sh.fb_bin;
-      nb += bits;
-      need -= sh.fb_above;
-      cnt = sh.fb_cnt;
-    }
-    unsigned long long Tc;
-    if (g == 0) sel_stamp(p, u, 2);
-    if ((p.debug & 16) && p.trace != nullptr && tid == 0 && g == 0) p.trace[(1 << 21) + (size_t)u * 8 + 7] = ncand;
-    if (listed) {  // narrow inside shared memory; candA stays intact for the part counts
-      const unsigned long long* src = candA;
-      unsigned long long* dst = candB;
-      while (cnt != need && ncand > 256) {
-        const int bits = min(8, 64 - nb);
-        for (int i = tid; i < (1 << bits); i += kPT) hist[i] = 0u;
-        __syncthreads();
-        for (int i = tid; i < ncand; i += kPT)
-          atomicAdd(&hist[(src[i] >> (64 - nb - bits)) & ((1ull << bits) - 1)], 1u);
-        __syncthreads();
-        find_bin(hist, 1 << bits, need, sh);
-        P = (P << bits) | (unsigned long long)sh.fb_bin;
-        nb += bits;
-        need -= sh.fb_above;
-        cnt = sh.fb_cnt;
-        if (cnt == need) break;
-        if (tid == 0) sh.ncand = 0;
-        __syncthreads();
-        for (int i0 = 0; i0 < ncand; i0 += kPT) {
-          const int i = i0 + tid;
-          const unsigned long long c = i < ncand ? src[i] : 0ull;
-          append_if(i < ncand && (c >> (64 - nb)) == P, c, dst, &sh.ncand);
-        }
-        __syncthreads();
-        ncand = sh.ncand;
-        src = dst;
-        dst = (dst == candB) ? candC : candB;
-      }
-      if (g == 0) sel_stamp(p, u, 3);
-      if (cnt == need) {
-        Tc = nb >= 64 ? P : (P << (64 - nb));
-      } else {  // <= 256 distinct candidates: the need-th largest by direct rank
-        for (int ci = tid; ci < ncand; ci += kPT) {
-          const unsigned long long c = src[ci];
-          unsigned rank = 0;
-          for (int i = 0; i < ncand; ++i) rank += src[i] > c;
-          if (rank == need - 1) sh.tsel = c;
-        }
-        __syncthreads();
-        Tc = sh.tsel;
-      }
-      if (offsets) {  // kept candidates per part
-        const int n0 = sh.ncand_first;
-        for (int i = tid; i < n0; i += kPT) {
-          const unsigned long long c = candA[i];
-          if (c >= Tc) atomicAdd(&poff[(int)(~(uint32_t)c) / Lh], 1u);
-        }
-      }
-    } else {
-      Tc = nb >= 64 ? P : (P << (64 - nb));
-      if (offsets) {  // counting pass: rows >= Tc per part
-        ks.start();
-        ks.run([&](int j0, const uint32_t* kc, int nrow) {
-          for (int i0 = 0; i0 < nrow; i0 += kPT) {
-            const int i = i0 + tid;
-            const bool on = i < nrow && comp_key(kc[i], j0 + i) >= Tc;
-            const int c = __popc(__ballot_sync(0xffffffffu, on));
-            if (lane == 0 && c) atomicAdd(&poff[(j0 + i0 + 32 * w) / Lh], (uint32_t)c);
-          }
-        });
-      }
-    }
-    if (g == 0) sel_stamp(p, u, 4);
-    if (tid == 0) p.tcs[(size_t)u * G + g] = Tc;
-    if (offsets) {  // counts -> exclusive offsets (one warp)
-      __syncthreads();
-      if (w == 0) {
-        unsigned run = 0;
-        for (int q0 = 0; q0 < nhp; q0 += 32) {
-          const int q = q0 + lane;
-          const unsigned v = q < nhp ? __ldcg(&poff[q]) : 0u;
-          unsigned x = v;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const unsigned t = __shfl_up_sync(0xffffffffu, x, off);
-            if (lane >= off) x += t;
-          }
-          if (q < nhp) poff[q] = run + x - v;
-          run += __shfl_sync(0xffffffffu, x, 31);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (tid == 0) cu[0] = 0u;  // A arrivals: ready for the next launch
-  sel_stamp(p, u, 5);
-  __syncthreads();
-  if (tid == 0) {  // the barrier makes every thread's writes visible to thread 0; its release publishes them
-    __threadfence();
-    st_release(&cu[2], 1u);
-  }
-  sel_stamp(p, u, 6);
-}
-
-// ------------------------------------------------------------------ item A
-template <typename T, int G_T, int VEC, int LPR1>
-__device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t* tile, int rows_here,
-                                             const float (&q1)[G_T][VEC], int G, uint32_t* keys0, uint32_t* kl,
-                                             float* approx0, uint32_t* hist, int HB, int hshift) {
-  constexpr int E = sizeof(T);
-  constexpr int RPW1 = 32 / LPR1;
-  constexpr int U = G_T >= 4 ? 2 : 4;  // independent rows in flight per lane (register budget: 2 CTAs / SM)
-  const int lane = lane_id();
-  const int row_bytes = p.dbox * E;
-  const int nch1 = p.dbox / VEC;
-  const int r = lane / LPR1, sl = lane % LPR1;
-  const bool lane_on = sl < nch1;
-  const int passes = p.r1 / RPW1;  // host: r1 % (U * RPW1) == 0
-  for (int ps = 0; ps < passes; ps += U) {
-    float x[U][VEC];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int rr = (ps + u) * RPW1 + r;
-      if (lane_on) lds_chunk<T, VEC>(tile + rr * row_bytes + sl * VEC * E, x[u]);
-      else
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) x[u][v] = 0.f;
-    }
-#pragma unroll
-    for (int g = 0; g < G_T; ++g) {
-      float acc[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        acc[u] = 0.f;
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[u] = fmaf(q1[g][v], x[u][v], acc[u]);
-        acc[u] = sum_lanes<LPR1>(acc[u]);
-      }
-      if (g < G) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int rr = (ps + u) * RPW1 + r;
-          if (sl == 0 && rr < rows_here) {
-            const uint32_t key = order_key(acc[u]);
-            keys0[(size_t)g * p.kstride + rr] = key;
-            if (kl != nullptr) kl[g * p.Lc + rr] = key;
-            if (approx0 != nullptr) approx0[(size_t)g * p.S_cap + rr] = acc[u];
-            atomicAdd(&hist[g * HB + (key >> hshift)], 1u);
-          }
-        }
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
-  unsigned long long d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ unsigned long long pk2(uint32_t lo, uint32_t hi) {
-  return ((unsigned long long)hi << 32) | lo;
-}
-
-// Phase-1 stage consumed by ONE warp with one lane per row (single query
-// head): RB-byte lead rows, TMA-swizzled (64 B: chunk ^ (row >> 1 & 3); 128 B:
-// chunk ^ (row & 7)) so the 16 B row reads are conflict-free; packed fp32 FMA
-// (two partial sums, any order is inside the fp32 tie band); the key and
-// approx stores are coalesced.
-template <typename T, int RB>
-__device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint8_t* tile, int rows_here,
-                                                 const unsigned long long (&q2)[32], uint32_t* keys0,
-                                                 uint32_t* kl, float* approx0, uint32_t* hist, int hshift) {
-  constexpr int NCH = RB / 16;
-  const int lane = lane_id();
-  for (int r0 = 0; r0 < p.r1; r0 += 64) {
-    uint4 v[2][NCH];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int rr = r0 + 32 * i + lane;
-      const int sw = RB == 64 ? ((rr >> 1) & 3) : (rr & 7);
-#pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        v[i][c] = *reinterpret_cast<const uint4*>(tile + rr * RB + ((c ^ sw) << 4));
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      unsigned long long acc = 0ull;
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const uint32_t wv[4] = {v[i][c].x, v[i][c].y, v[i][c].z, v[i][c].w};
-        if constexpr (sizeof(T) == 2) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc = ffma2(pk2(wv[e] << 16, wv[e] & 0xFFFF0000u), q2[c * 4 + e], acc);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) acc = ffma2(pk2(wv[2 * e], wv[2 * e + 1]), q2[c * 2 + e], acc);
-        }
-      }
-      const float sc = __uint_as_float((uint32_t)acc) + __uint_as_float((uint32_t)(acc >> 32));
-      const int rr = r0 + 32 * i + lane;
-      if (rr < rows_here) {
-        const uint32_t key = order_key(sc);
-        keys0[rr] = key;
-        if (kl != nullptr) kl[rr] = key;
-        if (approx0 != nullptr) approx0[rr] = sc;
-        atomicAdd(&hist[key >> hshift], 1u);
-      }
-    }
-  }
-}
-
-// Phase-1 stage consumed by ONE warp on the tensor cores (bf16 caches, query
-// groups G >= 2: scores[rows x G] = K_lead[rows x dbox] . Q[dbox x G] is a real
-// contraction).  q is split into three bf16 terms (hi + mid + lo == the fp32
-// value), one mma n-tile each, so a lane sums its own three fragments: the
-// scores carry fp32-level error, inside the tie band of the selection parity
-// (SURVEY 8c O4).  Lead rows are RB = 64 / 128 B, TMA-swizzled.  Lane
-// (g8, t4) holds rows {g8, g8 + 8} x heads {2 t4, 2 t4 + 1} of each 16-row block.
-template <int RB, int G_T>
-__device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint8_t* tile, int rows_here,
-                                                 const uint32_t (&qf)[3][4][2], int G, uint32_t* keys0,
-                                                 uint32_t* kl, float* approx0, uint32_t* hist, int HB, int hshift) {
-  constexpr int KS = RB / 32;  // k-steps of 16 bf16 columns
-  const int lane = lane_id();
-  const int g8 = lane >> 2, t4 = lane & 3;
-  const uint32_t tb = smem_u32(tile);
-  const int rA = (lane & 7) | (((lane >> 3) & 1) << 3);
-  const int cA = (lane >> 4) & 1;
-  for (int b0 = 0; b0 < p.r1; b0 += 16) {
-    float S[3][4];
-#pragma unroll
-    for (int t = 0; t < 3; ++t)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) S[t][i] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int r = b0 + rA, c = 2 * ks + cA;
-      const int sw = RB == 64 ? ((r >> 1) & 3) : (r & 7);
-      uint32_t a[4];
-      ldsm_x4(tb + (uint32_t)(r * RB + ((c ^ sw) << 4)), a);
-#pragma unroll
-      for (int t = 0; t < 3; ++t) mma_bf16(S[t], a, qf[t][ks][0], qf[t][ks][1]);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int rr = b0 + g8 + (i >> 1) * 8;
-      const int h = 2 * t4 + (i & 1);
-      if (h < G && rr < rows_here) {
-        const float sc = (S[0][i] + S[1][i]) + S[2][i];
-        const uint32_t key = order_key(sc);
-        keys0[(size_t)h * p.kstride + rr] = key;
-        if (kl != nullptr) kl[h * p.Lc + rr] = key;
-        if (approx0 != nullptr) approx0[(size_t)h * p.S_cap + rr] = sc;
-        atomicAdd(&hist[h * HB + (key >> hshift)], 1u);
-      }
-    }
-  }
-}
-
-template <typename T, int G_T, int VEC>
-__device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, int c, uint8_t* ring,
-                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, uint32_t* kloc, uint64_t* sbar,
-                       unsigned& sphase, RingPos& rp, PipeShared& sh) {
-  constexpr int E = sizeof(T);
-  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
-  const int nsw = p.nst, SB = p.stage_bytes;
-  const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G;
-  int S = p.lens[b];
-  S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
-  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
-  if (c >= nparts) return 0;  // past this unit's length: not an arrival
-  const int row0 = c * p.Lc;
-  const int n = max(0, min(S - row0, p.Lc));
-  const int HB = 1 << p.hbits, hshift = 32 - p.hbits;
-  for (int i = tid; i < G * HB; i += kPT) hist[i] = 0u;
-  __syncthreads();
-  if (n > 0) {
-    const int R1 = p.r1;
-    const int nbox = ceil_div(n, R1);
-    const unsigned box_bytes = (unsigned)(R1 * p.dbox * E);
-    const int mine = nbox > w ? ceil_div(nbox - w, kPW) : 0;  // boxes w, w + kPW, ...
-    auto issue = [&](int k, const RingPos& at) {
-      mbar_expect_tx(&wbar[at.slot], box_bytes);
-      tma_box4d(wring + at.slot * SB, lead_map, 0, row0 + (w + k * kPW) * R1, hk, b, &wbar[at.slot]);
-    };
-    if (lane == 0) {
-      RingPos q = rp;
-      for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
-    }
-    const size_t qrow0 = (size_t)b * p.Hq + (size_t)hk * G;
-    const int nch1 = p.dbox / VEC;
-    const int LPR1 = next_pow2(nch1);
-    const int sl = lane % LPR1;
-    float q1[G_T][VEC];
-#pragma unroll
-    for (int g = 0; g < G_T; ++g)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        const int col = sl * VEC + v;
-        q1[g][v] = (g < G && col < p.d && sl < nch1) ? p.q_hat[(qrow0 + g) * p.D + col] : 0.f;
-      }
-    uint32_t* keys_u = p.keys + (size_t)u * G * p.kstride + row0;
-    // spec: the chunk's keys also stay in shared memory ([G][Lc], the idle B-item entry region)
-    auto kl0 = [&](int box) -> uint32_t* { return p.spec ? kloc + box * p.r1 : nullptr; };
-    float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap + row0 : nullptr;
-    constexpr int E = sizeof(T);
-    bool consumed = false;
-    if constexpr (sizeof(T) == 2 && G_T >= 2) {
-      if (p.lead_swz != 0) {  // tensor-core scores for the query group
-        uint32_t qf[3][4][2];   // [part][k-step][reg]: B operand, k = 16 ks + 2 t4 + {0, 1, 8, 9}, n = head
-        const int g8 = lane >> 2, t4 = lane & 3;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          float v[4], r1v[4], r2v[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int dim = 16 * ks + 2 * t4 + (i & 1) + (i >> 1) * 8;
-            v[i] = (g8 < G && dim < p.d) ? p.q_hat[(qrow0 + g8) * p.D + dim] : 0.f;
-            r1v[i] = v[i] - bf16_hi(v[i]);
-            r2v[i] = r1v[i] - bf16_hi(r1v[i]);
-          }
-          qf[0][ks][0] = pack_bf16(v[0], v[1]);
-          qf[0][ks][1] = pack_bf16(v[2], v[3]);
-          qf[1][ks][0] = pack_bf16(r1v[0], r1v[1]);
-          qf[1][ks][1] = pack_bf16(r1v[2], r1v[3]);
-          qf[2][ks][0] = pack_bf16(r2v[0], r2v[1]);
-          qf[2][ks][1] = pack_bf16(r2v[2], r2v[3]);
-        }
-        for (int k = 0; k < mine; ++k, rp.advance(1)) {
-          mbar_wait(&wbar[rp.slot], rp.phase);
-          const uint8_t* tile = wring + rp.slot * SB;
-          const int i = w + k * kPW;
-          const int rows_here = min(R1, n - i * R1);
-          uint32_t* k0 = keys_u + i * R1;
-          float* a0 = approx_u ? approx_u + i * R1 : nullptr;
-          if (p.lead_swz == 64)
-            lead_consume_mma<64, G_T>(p, tile, rows_here, qf, G, k0, kl0(i), a0, hist, HB, hshift);
-          else
-            lead_consume_mma<128, G_T>(p, tile, rows_here, qf, G, k0, kl0(i), a0, hist, HB, hshift);
-          __syncwarp();
-          if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
-        }
-        consumed = true;
-      }
-    }
-    if (consumed || (sizeof(T) == 2 && G_T >= 2)) {  // (bf16 groups always take the tensor-core path: host)
-    } else if (G_T == 1 && p.lead_swz != 0) {  // one lane per row (swizzled lead rows)
-      constexpr int Q2 = 32;  // element pairs of the widest lead row (128 B of bf16)
-      unsigned long long q2[Q2];
-#pragma unroll
-      for (int j = 0; j < Q2; ++j) {
-        const int c0 = 2 * j, c1 = 2 * j + 1;
-        const float a = c0 < p.d ? p.q_hat[qrow0 * p.D + c0] : 0.f;
-        const float bq = c1 < p.d ? p.q_hat[qrow0 * p.D + c1] : 0.f;
-        q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
-      }
-      for (int k = 0; k < mine; ++k, rp.advance(1)) {
-        mbar_wait(&wbar[rp.slot], rp.phase);
-        const uint8_t* tile = wring + rp.slot * SB;
-        const int i = w + k * kPW;
-        const int rows_here = min(R1, n - i * R1);
-        uint32_t* k0 = keys_u + i * R1;
-        float* a0 = approx_u ? approx_u + i * R1 : nullptr;
-        if (p.lead_swz == 64)
-          lead_consume_lpr<T, 64>(p, tile, rows_here, q2, k0, kl0(i), a0, hist, hshift);
-        else
-          lead_consume_lpr<T, 128>(p, tile, rows_here, q2, k0, kl0(i), a0, hist, hshift);
-        __syncwarp();
-        if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
-      }
-    } else if constexpr (!(sizeof(T) == 2 && G_T >= 2))
-    for (int k = 0; k < mine; ++k, rp.advance(1)) {
-      mbar_wait(&wbar[rp.slot], rp.phase);
-      const uint8_t* tile = wring + rp.slot * SB;
-      const int i = w + k * kPW;
-      const int rows_here = min(R1, n - i * R1);
-      uint32_t* k0 = keys_u + i * R1;
-      float* a0 = approx_u ? approx_u + i * R1 : nullptr;
-      switch (LPR1) {
-        case 1: lead_consume<T, G_T, VEC, 1>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 2: lead_consume<T, G_T, VEC, 2>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 4: lead_consume<T, G_T, VEC, 4>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 8: lead_consume<T, G_T, VEC, 8>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 16: lead_consume<T, G_T, VEC, 16>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        default: lead_consume<T, G_T, VEC, 32>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-      }
-      __syncwarp();  // every lane is done with the slot before it is refilled
-      if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
-    }
-  }
-  __syncthreads();
-  if (p.spec && n > 0) {
-    // Speculative candidates (SURVEY 8(a) R7 made cheap): this chunk is a sample of the unit, so the
-    // unit's boundary bin is near the chunk's own k * n / S quantile.  Rows within kSpecW bins of
-    // it go to a per-(unit, head) list; the selection uses the list when every chunk's window holds
-    // the true boundary bin and falls back to scanning all keys otherwise.
-    const int kb = k_of(p, S);
-    const unsigned lt = (1u << lane) - 1u;
-    for (int g = 0; g < G; ++g) {
-      int kq = (int)(((long long)kb * n + S / 2) / S);
-      kq = kq < 1 ? 1 : (kq > n ? n : kq);
-      find_bin(hist + g * HB, HB, (unsigned)kq, sh);
-      const int lo = max(0, sh.fb_bin - kSpecW), hi = min(HB - 1, sh.fb_bin + kSpecW);
-      const size_t ug = (size_t)u * G + g;
-      if (tid == 0) p.cwin[ug * p.nA + c] = (uint32_t)lo | ((uint32_t)hi << 16);
-      unsigned long long* cb = p.cbuf + ug * p.ccap;
-      for (int j0 = 0; j0 < n; j0 += kPT) {
-        const int j = j0 + tid;
-        const uint32_t key = j < n ? kloc[g * p.Lc + j] : 0u;
-        const int bin = (int)(key >> hshift);
-        const bool m = j < n && bin >= lo && bin <= hi;
-        const unsigned bal = __ballot_sync(0xffffffffu, m);
-        unsigned base = 0;
-        if (lane == 0 && bal) base = atomicAdd(&p.ccnt[ug], (unsigned)__popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const unsigned at = base + __popc(bal & lt);
-        if (m && at < (unsigned)p.ccap) cb[at] = comp_key(key, row0 + j);
-      }
-    }
-  }
-  uint32_t* gh = p.hist + (size_t)u * G * HB;
-  for (int i = tid; i < G * HB; i += kPT) {
-    const uint32_t v = hist[i];
-    if (v) atomicAdd(&gh[i], v);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    sh.last = atomicAdd(&p.ctrl[2 + 4 * (size_t)u], 1u) == (unsigned)nparts - 1u;
-    if (sh.last) __threadfence();
-  }
-  __syncthreads();
-  if (sh.last) {
-    if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();
-    select_unit<G_T>(p, u, S, ring, hist, sbar, sphase, sh);
-    return 3;
-  }
-  return 1;
-}
-
-// ------------------------------------------------------------------ item B
-template <int G_T>
-__device__ void merge_unit(const PipeParams& p, int u, int S, PipeShared& sh) {
-  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
-  const int G = p.G, D = p.D, ldp = D + 2;
-  uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
-  const size_t qrow0 = ((size_t)(u / p.Hkv) * p.Hq) + (size_t)(u % p.Hkv) * G;
-  const bool split = u + p.lag >= p.units;  // tail units run half-size B items
-  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc) * (split ? 2 : 1);
-  const float* part = p.part + (size_t)u * 2 * p.nA * G * ldp;
-  for (int i = tid; i < G * D; i += kPT) {
-    const int g = i / D, col = i % D;
-    float mm = -CUDART_INF_F, ll = 0.f, aa = 0.f;
-    for (int q = 0; q < nparts; ++q) {
-      const float* f = part + ((size_t)q * G + g) * ldp;
-      float s1, s2;
-      merge_state(mm, ll, __ldcg(&f[D]), __ldcg(&f[D + 1]), s1, s2);
-      aa = aa * s1 + __ldcg(&f[col]) * s2;
-    }
-    p.out[(qrow0 + g) * D + col] = ll > 0.f ? aa / ll : 0.f;
-    if (col == 0) {
-      sh.gm[g] = mm;
-      sh.gl[g] = ll;
-    }
-  }
-  __syncthreads();
-  if (p.weights_out != nullptr) {  // softmax weights of each head's selection, ascending rows
-    const unsigned lt = (1u << lane) - 1u;
-    for (int g = 0; g < G; ++g) {
-      const unsigned long long Tc = __ldcg(&p.tcs[(size_t)u * G + g]);
-      const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
-      const float M = sh.gm[g], invL = 1.f / sh.gl[g];
-      const float* lg = p.logits + ((size_t)u * G + g) * p.S_cap;
-      float* dst = p.weights_out + (qrow0 + g) * p.idx_stride;
-      unsigned emitted = 0;
-      for (int j0 = 0; j0 < S; j0 += kPT) {
-        const int j = j0 + tid;
-        const bool on = j < S && comp_key(__ldcg(&keys[j]), j) >= Tc;
-        const unsigned bal = __ballot_sync(0xffffffffu, on);
-        if (lane == 0) sh.wcnt[w][0] = __popc(bal);
-        __syncthreads();
-        unsigned before = 0, tot = 0;
-        for (int ww = 0; ww < kPW; ++ww) {
-          before += ww < w ? sh.wcnt[ww][0] : 0;
-          tot += sh.wcnt[ww][0];
-        }
-        if (on) dst[emitted + before + __popc(bal & lt)] = exp2f(__ldcg(&lg[j]) - M) * invL;
-        emitted += tot;
-        __syncthreads();
-      }
-    }
-  }
-  if (tid == 0) {
-    cu[1] = 0u;
-    cu[2] = 0u;
-  }
-}
-
-template <typename T, int G_T, int VEC, int D_T>
-__device__ void stream_B_simt(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u,
-                              int n, int row_base, size_t qrow0, const uint32_t* ents, const float* apx, uint8_t* wring,
-                              uint64_t* wbar, RingPos& rp, float* wpart) {
-  constexpr int E = sizeof(T);
-  constexpr int LPR3 = D_T / VEC;  // lanes per V row
-  constexpr int RPW3 = 32 / LPR3;
-  constexpr int ROWB = D_T * E;
-  const int lane = lane_id(), w = warp_id();
-  const int nsw = p.nst, SB = p.stage_bytes;
-  const int G = p.G, D = D_T;
-  const bool split = p.split_k != 0;
-  const int kcol0 = split ? p.d : 0;  // first gathered K column
-  const int KW = D - kcol0;           // gathered K columns
-  const int KROWB = KW * E;
-  const int R3 = p.r3;
-  const int nstage = ceil_div(n, R3);
-  const unsigned stage_bytes = (unsigned)(R3 * (KROWB + ROWB));
-  const bool want_logits = p.weights_out != nullptr;
-  const int mine = nstage > w ? ceil_div(nstage - w, kPW) : 0;  // stages w, w + kPW, ...
-  auto issue = [&](int k, const RingPos& at) {
-    const int st = w + k * kPW;
-    uint8_t* dst = wring + at.slot * SB;
-    if (lane == 0) mbar_expect_tx(&wbar[at.slot], stage_bytes);
-    int row = -1;  // lane t < R3 resolves row t of the stage; -1 = out of bounds, zero-filled
-    const int t = st * R3 + lane;
-    if (lane < R3 && t < n) row = row_base + (int)(ents[t] & 0xFFFFFFu);
-    for (int qq = 0; qq < R3 / 4; ++qq) {
-      const int a0 = __shfl_sync(0xffffffffu, row, 4 * qq);
-      const int a1 = __shfl_sync(0xffffffffu, row, 4 * qq + 1);
-      const int a2 = __shfl_sync(0xffffffffu, row, 4 * qq + 2);
-      const int a3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
-      if (lane == 0) {
-        tma_gather4(dst + qq * 4 * KROWB, krow_map, kcol0, a0, a1, a2, a3, &wbar[at.slot]);
-        tma_gather4(dst + R3 * KROWB + qq * 4 * ROWB, vrow_map, 0, a0, a1, a2, a3, &wbar[at.slot]);
-      }
-    }
-  };
-  {
-    RingPos qp = rp;
-    for (int k = 0; k < nsw && k < mine; ++k, qp.advance(1)) issue(k, qp);
-  }
-  float acc[G_T][VEC];
-  float m[G_T], l[G_T];
-#pragma unroll
-  for (int g = 0; g < G_T; ++g) {
-    m[g] = -CUDART_INF_F;
-    l[g] = 0.f;
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[g][v] = 0.f;
-  }
-  const int r = lane / LPR3, sl = lane % LPR3;
-  const bool k_on = sl * VEC < KW;
-  float q3[G_T][VEC];
-#pragma unroll
-  for (int g = 0; g < G_T; ++g)
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const int col = kcol0 + sl * VEC + v;
-      q3[g][v] = (g < G && k_on && col < D) ? p.q_hat[(qrow0 + g) * D + col] * p.qscale : 0.f;
-    }
-  constexpr int U = 2;  // rows per lane slot whose logits are formed before the softmax updates
-  for (int k = 0; k < mine; ++k, rp.advance(1)) {
-    mbar_wait(&wbar[rp.slot], rp.phase);
-    const int st = w + k * kPW;
-    const uint8_t* kt = wring + rp.slot * SB;
-    const uint8_t* vt = kt + R3 * KROWB;
-    for (int ps = 0; ps < R3 / RPW3; ps += U) {  // host: (R3 / RPW3) % U == 0
-      float x[U][G_T];
-      int jr[U];
-      unsigned msk[U];
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        const int rr = (ps + uu) * RPW3 + r;
-        const int t = st * R3 + rr;
-        const bool ok = t < n;
-        const uint32_t e = ok ? ents[t] : 0u;
-        jr[uu] = (int)(e & 0xFFFFFFu);
-        msk[uu] = e >> 24;
-        float kx[VEC];
-        if (k_on) lds_chunk<T, VEC>(kt + rr * KROWB + sl * VEC * E, kx);
-        else
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) kx[v] = 0.f;
-#pragma unroll
-        for (int g = 0; g < G_T; ++g) {
-          float s = 0.f;
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) s = fmaf(q3[g][v], kx[v], s);
-          s = sum_lanes<LPR3>(s);
-          if (split && ok && g < G) s += apx[g * p.Lc + t];
-          x[uu][g] = s;
-        }
-      }
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu) {
-        const int rr = (ps + uu) * RPW3 + r;
-        float vx[VEC];
-        lds_chunk<T, VEC>(vt + rr * ROWB + sl * VEC * E, vx);
-#pragma unroll
-        for (int g = 0; g < G_T; ++g) {
-          if (msk[uu] & (1u << g)) {
-            const float xv = x[uu][g];
-            if (want_logits && sl == 0) p.logits[((size_t)u * G + g) * p.S_cap + jr[uu]] = xv;
-            const float mn = fmaxf(m[g], xv);
-            const float sc = exp2f(m[g] - mn);
-            const float pe = exp2f(xv - mn);
-            l[g] = l[g] * sc + pe;
-            m[g] = mn;
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[g][v] = fmaf(pe, vx[v], acc[g][v] * sc);
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (k + nsw < mine) issue(k + nsw, rp);
-  }
-
-  // merge lanes sharing columns, then warps in fixed order, into this part's state
-#pragma unroll
-  for (int g = 0; g < G_T; ++g) {
-    for (int off = LPR3; off < 32; off <<= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m[g], off);
-      const float l2 = __shfl_xor_sync(0xffffffffu, l[g], off);
-      float s1, s2;
-      merge_state(m[g], l[g], m2, l2, s1, s2);
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        const float a2 = __shfl_xor_sync(0xffffffffu, acc[g][v], off);
-        acc[g][v] = acc[g][v] * s1 + a2 * s2;
-      }
-    }
-  }
-  const int ldp = D + 2;
-  __syncthreads();
-  if (r == 0) {
-#pragma unroll
-    for (int g = 0; g < G_T; ++g) {
-      if (g >= G) break;
-      float* dstp = wpart + ((size_t)w * G_T + g) * ldp;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) dstp[sl * VEC + v] = acc[g][v];
-      if (sl == 0) {
-        dstp[D] = m[g];
-        dstp[D + 1] = l[g];
-      }
-    }
-  }
-}
-
-// Phase 3 on the tensor cores (bf16 caches).  A stage is 8 gathered rows
-// (4 KB at D = 128: many small stages keep 16 warps per SM issuing gathers,
-// tools/gatherbench.cu): K and V as 128 B row halves, 128B-swizzled by TMA so
-// ldmatrix is conflict-free.  Per stage, with the 8 rows as M rows 0..7 of
-// m16n8k16 (rows 8..15 zero):  S^T[8 x 8] = K[8 x D] . Qc[D x 8]  and
-// O^T[D x 8] += V^T[D x 8] . P^T[8 x 8]  (fp32 accumulate).  Columns carry
-// (head, hi / lo part): q * qscale and the softmax weights are split into two
-// bf16 terms, so both products keep ~2^-17 relative accuracy.
-// G <= 4: column 2h + part;  G == 8: columns = heads, hi and lo in two mmas.
-template <int G_T, int D_T>
-__device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u,
-                             int n, int row_base, size_t qrow0, const uint32_t* ents, uint8_t* wring, uint64_t* wbar,
-                             RingPos& rp, float* wpart) {
-  constexpr int NH = D_T / 64;             // 128 B row halves
-  constexpr int KS = D_T / 16;             // k-steps of q.K == m-tiles of P.V
-  constexpr int R = 8;                     // rows per stage
-  constexpr int HW = R * 128;              // bytes of one half block (one swizzle atom)
-  constexpr int NHL = G_T == 8 ? 2 : 1;    // heads per lane
-  constexpr bool kSplitCols = G_T < 8;
-  const int lane = lane_id(), w = warp_id();
-  const int G = p.G;
-  const int nsw = p.nst, SB = p.stage_bytes;
-  const int g8 = lane >> 2, t4 = lane & 3;
-  const int nstage = ceil_div(n, R);
-  const unsigned stage_bytes = (unsigned)(R * D_T * 2 * 2);
-  const bool want_logits = p.weights_out != nullptr;
-  const int mine = nstage > w ? ceil_div(nstage - w, kPW) : 0;  // stages w, w + kPW, ...
-  auto issue = [&](int k, const RingPos& at) {
-    const int st = w + k * kPW;
-    uint8_t* dst = wring + at.slot * SB;
-    if (lane == 0) mbar_expect_tx(&wbar[at.slot], stage_bytes);
-    int row = -1;  // -1: out of bounds, zero-filled
-    const int t = st * R + lane;
-    if (lane < R && t < n) row = row_base + (int)(ents[t] & 0xFFFFFFu);
-#pragma unroll
-    for (int qq = 0; qq < R / 4; ++qq) {
-      const int a0 = __shfl_sync(0xffffffffu, row, 4 * qq);
-      const int a1 = __shfl_sync(0xffffffffu, row, 4 * qq + 1);
-      const int a2 = __shfl_sync(0xffffffffu, row, 4 * qq + 2);
-      const int a3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
-      if (lane == 0) {
-#pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          tma_gather4(dst + h * HW + qq * 512, krow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
-          tma_gather4(dst + (NH + h) * HW + qq * 512, vrow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
-        }
-      }
-    }
-  };
-  {
-    RingPos qp = rp;
-    for (int k = 0; k < nsw && k < mine; ++k, qp.advance(1)) issue(k, qp);
-  }
-  // B operand of S^T = K . Qc: lane holds Qc[16 ks + 2 t4 + {0, 1, 8, 9}][g8]
-  uint32_t qb[KS][2], ql[G_T == 8 ? KS : 1][2];
-#pragma unroll
-  for (int ks = 0; ks < KS; ++ks) {
-    const int k0 = 16 * ks + 2 * t4;
-    const int head = kSplitCols ? (g8 >> 1) : g8;
-    float v[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int dim = k0 + (i & 1) + (i >> 1) * 8;
-      v[i] = head < G ? p.q_hat[(qrow0 + head) * D_T + dim] * p.qscale : 0.f;
-    }
-    if (kSplitCols) {
-      const bool lo = g8 & 1;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = lo ? bf16_lo(v[i]) : v[i];
-      qb[ks][0] = pack_bf16(v[0], v[1]);
-      qb[ks][1] = pack_bf16(v[2], v[3]);
-    } else {
-      qb[ks][0] = pack_bf16(v[0], v[1]);
-      qb[ks][1] = pack_bf16(v[2], v[3]);
-      ql[ks][0] = pack_bf16(bf16_lo(v[0]), bf16_lo(v[1]));
-      ql[ks][1] = pack_bf16(bf16_lo(v[2]), bf16_lo(v[3]));
-    }
-  }
-  float O[KS][4];
-#pragma unroll
-  for (int mt = 0; mt < KS; ++mt)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) O[mt][i] = 0.f;
-  float m[NHL], l[NHL];
-#pragma unroll
-  for (int j = 0; j < NHL; ++j) {
-    m[j] = -CUDART_INF_F;
-    l[j] = 0.f;
-  }
-  const int rX = lane & 7;            // ldmatrix.x2 row (lanes 0..15 address two 8x8 matrices)
-  const int cX = (lane >> 3) & 1;     // second matrix: +8 columns (K) / +8 dims (V)
-  for (int k = 0; k < mine; ++k, rp.advance(1)) {
-    mbar_wait(&wbar[rp.slot], rp.phase);
-    const int st = w + k * kPW;
-    const uint32_t sb = smem_u32(wring + rp.slot * SB);
-    float S[4] = {0.f, 0.f, 0.f, 0.f}, S2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t a2[2];
-      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
-                   : "=r"(a2[0]), "=r"(a2[1])
-                   : "r"(swz128(sb + (ks >> 2) * HW, rX, ((ks & 3) << 1) | cX)));
-      const uint32_t a[4] = {a2[0], 0u, a2[1], 0u};
-      mma_bf16(S, a, qb[ks][0], qb[ks][1]);
-      if (!kSplitCols) mma_bf16(S2, a, ql[ks][0], ql[ks][1]);
-    }
-    const int tA = st * R + g8;
-    const uint32_t eA = tA < n ? ents[tA] : 0u;
-    float x[NHL], pr[NHL], sc[NHL];
-#pragma unroll
-    for (int j = 0; j < NHL; ++j) {
-      const int head = kSplitCols ? t4 : 2 * t4 + j;
-      x[j] = kSplitCols ? S[0] + S[1] : S[j] + S2[j];
-      const bool ok = head < G && ((eA >> (24 + head)) & 1u);
-      float tm = ok ? x[j] : -CUDART_INF_F;
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
-      tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
-      const float mn = fmaxf(m[j], tm);
-      sc[j] = (mn == -CUDART_INF_F) ? 1.f : exp2f(m[j] - mn);
-      pr[j] = ok ? exp2f(x[j] - mn) : 0.f;
-      l[j] = l[j] * sc[j] + pr[j];
-      m[j] = mn;
-      if (want_logits && ok) p.logits[((size_t)u * G + head) * p.S_cap + (eA & 0xFFFFFFu)] = x[j];
-    }
-    bool same = true;
-#pragma unroll
-    for (int j = 0; j < NHL; ++j) same &= sc[j] == 1.f;
-    if (!__all_sync(0xffffffffu, same)) {
-#pragma unroll
-      for (int mt = 0; mt < KS; ++mt) {
-        O[mt][0] *= sc[0];
-        O[mt][2] *= sc[0];
-        O[mt][1] *= sc[NHL - 1];
-        O[mt][3] *= sc[NHL - 1];
-      }
-    }
-    // B operand P^T: lane holds P[rows 2 t4, 2 t4 + 1][column g8] (rows 8..15 do not exist);
-    // (row r, lane head slot) lives in lane r * 4 + head slot
-    const int src0 = (2 * t4) * 4 + (g8 >> 1), src1 = src0 + 4;
-    uint32_t pb, pl = 0u;
-    if (kSplitCols) {
-      const float v0 = __shfl_sync(0xffffffffu, pr[0], src0);
-      const float v1 = __shfl_sync(0xffffffffu, pr[0], src1);
-      const bool lo = g8 & 1;
-      pb = pack_bf16(lo ? bf16_lo(v0) : v0, lo ? bf16_lo(v1) : v1);
-    } else {
-      const bool odd = g8 & 1;  // column g8 = head; element j = head & 1 of the source lane
-      const float a0 = __shfl_sync(0xffffffffu, pr[0], src0), b0 = __shfl_sync(0xffffffffu, pr[NHL - 1], src0);
-      const float a1 = __shfl_sync(0xffffffffu, pr[0], src1), b1 = __shfl_sync(0xffffffffu, pr[NHL - 1], src1);
-      const float v0 = odd ? b0 : a0, v1 = odd ? b1 : a1;
-      pb = pack_bf16(v0, v1);
-      pl = pack_bf16(bf16_lo(v0), bf16_lo(v1));
-    }
-#pragma unroll
-    for (int mt = 0; mt < KS; ++mt) {
-      const int dim = 16 * mt + (cX << 3);
-      uint32_t a2[2];
-      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
-                   : "=r"(a2[0]), "=r"(a2[1])
-                   : "r"(swz128(sb + (NH + (dim >> 6)) * HW, rX, (dim & 63) >> 3)));
-      const uint32_t a[4] = {a2[0], a2[1], 0u, 0u};
-      mma_bf16(O[mt], a, pb, 0u);
-      if (!kSplitCols) mma_bf16(O[mt], a, pl, 0u);
-    }
-    __syncwarp();
-    if (k + nsw < mine) issue(k + nsw, rp);
-  }
-#pragma unroll
-  for (int j = 0; j < NHL; ++j) {
-    l[j] += __shfl_xor_sync(0xffffffffu, l[j], 4);
-    l[j] += __shfl_xor_sync(0xffffffffu, l[j], 8);
-    l[j] += __shfl_xor_sync(0xffffffffu, l[j], 16);
-  }
-  __syncthreads();  // wpart aliases the ring: every warp has drained its slots
-#pragma unroll
-  for (int j = 0; j < NHL; ++j) {
-    const int head = kSplitCols ? t4 : 2 * t4 + j;
-    if (head < G) {
-      float* dstp = wpart + ((size_t)w * G_T + head) * (D_T + 2);
-#pragma unroll
-      for (int mt = 0; mt < KS; ++mt) {
-        if (kSplitCols) {
-          dstp[16 * mt + g8] = O[mt][0] + O[mt][1];
-          dstp[16 * mt + g8 + 8] = O[mt][2] + O[mt][3];
-        } else {
-          dstp[16 * mt + g8] = O[mt][j];
-          dstp[16 * mt + g8 + 8] = O[mt][2 + j];
-        }
-      }
-      if (g8 == 0) {
-        dstp[D_T] = m[j];
-        dstp[D_T + 1] = l[j];
-      }
-    }
-  }
-}
-
-// B(u, q): rows [q * Lc, (q + 1) * Lc).  kNB 128-row blocks per warp.
-template <typename T, int G_T, int VEC, int D_T, bool BIG>
-__device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u, int q,
-                      int half, uint8_t* ring, uint8_t* wring, uint64_t* wbar, uint32_t* ents, RingPos& rp,
-                      PipeShared& sh) {
-  constexpr int E = sizeof(T);
-  constexpr int LPR3 = D_T / VEC;  // lanes per V row
-  constexpr int RPW3 = 32 / LPR3;
-  constexpr int ROWB = D_T * E;
-  constexpr int NBG = BIG ? 2 * LOKI_PIPE_NB : LOKI_PIPE_NB;  // 128-row blocks per warp at G = 1
-  constexpr int kNB = G_T >= NBG ? 1 : NBG / G_T;  // Lc == kNB * 128 * kPW (host)
-  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
-  const int nsw = p.nst, SB = p.stage_bytes;
-  const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G, D = D_T;
-  int S = p.lens[b];
-  S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
-  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
-  if (q >= nparts) return 0;  // past this unit's length: not an arrival
-  // full part q = rows [q Lc, (q + 1) Lc); the tail units' half parts (half = 0 / 1) cover Lc / 2 rows each
-  const int span = half < 0 ? p.Lc : p.Lc / 2;
-  const int row0 = q * p.Lc + (half > 0 ? span : 0);
-  const int nrows = max(0, min(S - row0, span));
-  const int pidx = half < 0 ? q : 2 * q + half;             // partial-state slot
-  const int narrive = half < 0 ? nparts : 2 * nparts;     // B items of this unit
-  uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
-  if (tid == 0) {
-    unsigned long long spins = 0;
-    while (ld_acquire(&cu[2]) == 0u) {
-      __nanosleep(64);
-      if (++spins > (1ull << 28)) {
-        printf("loki pipe: unit %d never became ready (block %d)\n", u, (int)blockIdx.x);
-        __trap();
-      }
-    }
-  }
-  if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();  // ready observed (trace: wait vs work)
-  __syncthreads();
-  const bool split = p.split_k != 0;
-  const size_t qrow0 = (size_t)b * p.Hq + (size_t)hk * G;
-  float* apx = reinterpret_cast<float*>(ents + p.Lc);  // [G][Lc] phase-1 partial logits, log2 domain
-  // this part's selected rows, ascending, with head masks: one L2 round trip for the keys
-  int n = 0;
-  if (nrows > 0) {
-    const uint32_t* kbase = p.keys + (size_t)u * G * p.kstride;
-    unsigned long long Tc[G_T];
-#pragma unroll
-    for (int g = 0; g < G_T; ++g) Tc[g] = g < G ? __ldcg(&p.tcs[(size_t)u * G + g]) : ~0ull;
-    const int wr0 = row0 + w * kNB * 128;  // this warp's rows [wr0, wr0 + kNB * 128)
-    const int rend = row0 + nrows;
-    uint4 kk[kNB][G_T];
-#pragma unroll
-    for (int bq = 0; bq < kNB; ++bq) {
-      const int jb = wr0 + bq * 128 + 4 * lane;
-#pragma unroll
-      for (int g = 0; g < G_T; ++g)
-        kk[bq][g] = (g < G && jb < rend) ? ld_keys4(kbase + (size_t)g * p.kstride, jb) : make_uint4(0u, 0u, 0u, 0u);
-    }
-    unsigned m[kNB][4];
-    int ns = 0;
-#pragma unroll
-    for (int bq = 0; bq < kNB; ++bq)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = wr0 + bq * 128 + 4 * lane + e;
-        unsigned mm = 0;
-#pragma unroll
-        for (int g = 0; g < G_T; ++g)
-          if (g < G && j < rend && comp_key(u4_at(kk[bq][g], e), j) >= Tc[g]) mm |= 1u << g;
-        m[bq][e] = mm;
-        ns += mm != 0;
-      }
-    int wtot;
-    const int lpos = warp_excl_scan(ns, &wtot);
-    if (lane == 0) sh.wcnt[w][0] = wtot;
-    __syncthreads();
-    int pos = lpos;
-    for (int ww = 0; ww < kPW; ++ww) {
-      pos += ww < w ? sh.wcnt[ww][0] : 0;
-      n += sh.wcnt[ww][0];
-    }
-    // lane order inside a warp: block-major (bq), then lane, then e
-    int bpos[kNB];
-    {
-      int acc = 0;
-#pragma unroll
-      for (int bq = 0; bq < kNB; ++bq) {
-        int c = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) c += m[bq][e] != 0;
-        int tot;
-        const int ex = warp_excl_scan(c, &tot);
-        bpos[bq] = pos - lpos + acc + ex;  // warp base + earlier blocks + earlier lanes
-        acc += tot;
-      }
-    }
-#pragma unroll
-    for (int bq = 0; bq < kNB; ++bq) {
-      int qd = bpos[bq];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (m[bq][e]) {
-          const int j = wr0 + bq * 128 + 4 * lane + e;
-          ents[qd] = (m[bq][e] << 24) | (uint32_t)j;
-          if (split)
-#pragma unroll
-            for (int g = 0; g < G_T; ++g)
-              if (g < G) apx[g * p.Lc + qd] = key_to_float(u4_at(kk[bq][g], e)) * p.qscale;
-          ++qd;
-        }
-      }
-    }
-    if (p.idx_out != nullptr) {  // per-head ascending indices at the part's published offset
-#pragma unroll
-      for (int g = 0; g < G_T; ++g) {
-        if (g >= G) break;
-        int cg = 0;
-#pragma unroll
-        for (int bq = 0; bq < kNB; ++bq)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) cg += (m[bq][e] >> g) & 1u;
-        const int gtot = __reduce_add_sync(0xffffffffu, cg);
-        if (lane == 0) sh.wcnt[w][1 + g] = gtot;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int g = 0; g < G_T; ++g) {
-        if (g >= G) break;
-        int base = (int)__ldcg(&p.poff[((size_t)u * G + g) * 2 * p.nA + row0 / (p.Lc / 2)]);
-        for (int ww = 0; ww < w; ++ww) base += sh.wcnt[ww][1 + g];
-        int32_t* dst = p.idx_out + (qrow0 + g) * p.idx_stride;
-#pragma unroll
-        for (int bq = 0; bq < kNB; ++bq) {
-          int c = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) c += (m[bq][e] >> g) & 1u;
-          int tot;
-          int qd = base + warp_excl_scan(c, &tot);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if ((m[bq][e] >> g) & 1u) dst[qd++] = wr0 + bq * 128 + 4 * lane + e;
-          base += tot;
-        }
-      }
-    }
-  }
-  __syncthreads();
-
-  const int ldp = D + 2;
-  float* wpart = reinterpret_cast<float*>(ring);  // [kPW][G_T][D + 2]; every ring slot has been consumed
-  const int row_base = (int)(((long long)b * p.Hkv + hk) * p.unit_rows);
-  if constexpr (sizeof(T) == 2)  // bf16: always the tensor-core phase 3 (host sets p.mma)
-    stream_B_mma<G_T, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, wring, wbar, rp, wpart);
-  else
-    stream_B_simt<T, G_T, VEC, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, apx, wring, wbar, rp, wpart);
-  __syncthreads();
-  float* gpart = p.part + (((size_t)u * 2 * p.nA + pidx) * G) * ldp;
-  for (int i = tid; i < G * ldp; i += kPT) {
-    const int g = i / ldp, col = i % ldp;
-    float mm = -CUDART_INF_F, ll = 0.f, aa = 0.f;
-    for (int ww = 0; ww < kPW; ++ww) {
-      const float* src = wpart + ((size_t)ww * G_T + g) * ldp;
-      float s1, s2;
-      merge_state(mm, ll, src[D], src[D + 1], s1, s2);
-      if (col < D) aa = aa * s1 + src[col] * s2;
-    }
-    gpart[(size_t)g * ldp + col] = col < D ? aa : (col == D ? mm : ll);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    sh.last = atomicAdd(&cu[1], 1u) == (unsigned)narrive - 1u;
-    if (sh.last) __threadfence();
-  }
-  __syncthreads();
-  if (sh.last) {
-    if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();
-    merge_unit<G_T>(p, u, S, sh);
-    return 4;
-  }
-  return 2;
-}
-
-// ------------------------------------------------------------------ kernel
-template <typename T, int G_T, int VEC, int D_T, bool BIG>
-__global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
-                                                          const __grid_constant__ CUtensorMap lead_map,
-                                                          const __grid_constant__ CUtensorMap krow_map,
-                                                          const __grid_constant__ CUtensorMap vrow_map) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  __shared__ PipeShared sh;
-  // 1024 B alignment: the tensor-core path reads 128B-swizzled TMA tiles
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
-  const int nsw = p.nst;
-  uint8_t* ring = smem + p.off_ring;
-  uint8_t* wring = ring + (size_t)w * nsw * p.stage_bytes;
-  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bars) + (size_t)w * nsw;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + p.off_hist);
-  uint32_t* ents = reinterpret_cast<uint32_t*>(smem + p.off_ents);
-  uint64_t* sbar = reinterpret_cast<uint64_t*>(smem + p.off_bars) + (size_t)kPW * nsw;  // selection key stream
-  unsigned sphase = 0u;
-  if (lane == 0) {
-    for (int s = 0; s < nsw; ++s) mbar_init(&wbar[s], 1);
-    if (w == 0) {
-      mbar_init(&sbar[0], 1);
-      mbar_init(&sbar[1], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (tid == 0) {
-    prefetch_desc(&lead_map);
-    prefetch_desc(&krow_map);
-    prefetch_desc(&vrow_map);
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended rows are visible
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (tid == 0) sh.next_ticket = atomicAdd(&p.ctrl[0], 1u);
-  __syncthreads();
-  RingPos rp(nsw);
-  const int per_slot = 2 * p.nA;  // A(u, 0..nA-1) then B(u - lag, 0..nA-1); tail slots: half B items
-  for (;;) {
-    const unsigned t = sh.next_ticket;
-    __syncthreads();
-    if ((long long)t >= p.n_tickets) {
-      if (tid == 0 && atomicAdd(&p.ctrl[1], 1u) == gridDim.x - 1u) {  // last CTA out resets the counters
-        atomicExch(&p.ctrl[0], 0u);
-        atomicExch(&p.ctrl[1], 0u);
-      }
-      break;
-    }
-    if (tid == 0) sh.next_ticket = atomicAdd(&p.ctrl[0], 1u);  // prefetched; read after the item's barriers
-    const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
-    const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
-    int kind = 0;
-    if (slot >= p.units) {  // tail slot: no A items left, all 2 nA tickets are half-size B items
-      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
-                                      rp, sh);
-    } else if (r < p.nA) {
-      kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, sbar, sphase, rp, sh);
-    } else if (slot >= p.lag) {
-      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
-                                      rp, sh);
-    }
-    fence_proxy_async();  // this item's generic shared-memory writes precede the next item's TMA writes
-    __syncthreads();
-    if (p.trace != nullptr && tid == 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      long long* tr = p.trace + (size_t)t * 4;
-      tr[0] = t0;
-      tr[1] = globaltimer();
-      tr[2] = (long long)smid | ((long long)kind << 16) | ((long long)blockIdx.x << 32);
-      tr[3] = (kind >= 2) ? sh.t_sel : 0;
-    }
-  }
-}
-
-}  // namespace
-
-// ---------------------------------------------------------------- host side
 
 int pipe_warps() { return kPW; }
 int pipe_nb() { return LOKI_PIPE_NB; }
@@ -1564,90 +40,33 @@ size_t pipe_layout(int G_T, PipeParams* p) {
   return off;
 }
 
-template <typename T, int G_T, int VEC, int D_T, bool BIG>
-static cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st) {
-  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG>;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kPT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps);
-  return cudaLaunchKernelEx(&cfg, kern, p, m[0], m[1], m[2]);
-}
-
-template <typename T, int G_T, int VEC, int D_T, bool BIG>
-static int occupancy_t(size_t smem) {
-  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kPT, smem) != cudaSuccess) return 0;
-  return n;
-}
-
-// dispatch over (dtype, D, G_T); F is a functor template taking <T, G_T, VEC, D_T>
-#define LOKI_PIPE_DISPATCH(DTYPE, D, GT, CALL)                                                     \
-  do {                                                                                             \
-    if ((DTYPE) == LOKI_DTYPE_BF16) {                                                              \
-      switch ((D) * 16 + (GT)) {                                                                   \
-        case 64 * 16 + 1: return CALL(__nv_bfloat16, 1, 8, 64);                                    \
-        case 64 * 16 + 2: return CALL(__nv_bfloat16, 2, 8, 64);                                    \
-        case 64 * 16 + 4: return CALL(__nv_bfloat16, 4, 8, 64);                                    \
-        case 64 * 16 + 8: return CALL(__nv_bfloat16, 8, 4, 64);                                    \
-        case 128 * 16 + 1: return CALL(__nv_bfloat16, 1, 8, 128);                                  \
-        case 128 * 16 + 2: return CALL(__nv_bfloat16, 2, 8, 128);                                  \
-        case 128 * 16 + 4: return CALL(__nv_bfloat16, 4, 8, 128);                                  \
-        case 128 * 16 + 8: return CALL(__nv_bfloat16, 8, 4, 128);                                  \
-        case 256 * 16 + 1: return CALL(__nv_bfloat16, 1, 8, 256);                                  \
-        case 256 * 16 + 2: return CALL(__nv_bfloat16, 2, 8, 256);                                  \
-        case 256 * 16 + 4: return CALL(__nv_bfloat16, 4, 8, 256);                                  \
-        default: break;                                                                            \
-      }                                                                                            \
-    } else {                                                                                       \
-      switch ((D) * 16 + (GT)) {                                                                   \
-        case 64 * 16 + 1: return CALL(float, 1, 4, 64);                                            \
-        case 64 * 16 + 2: return CALL(float, 2, 4, 64);                                            \
-        case 64 * 16 + 4: return CALL(float, 4, 4, 64);                                            \
-        case 64 * 16 + 8: return CALL(float, 8, 4, 64);                                            \
-        case 128 * 16 + 1: return CALL(float, 1, 4, 128);                                          \
-        case 128 * 16 + 2: return CALL(float, 2, 4, 128);                                          \
-        case 128 * 16 + 4: return CALL(float, 4, 4, 128);                                          \
-        case 128 * 16 + 8: return CALL(float, 8, 4, 128);                                          \
-        default: break;                                                                            \
-      }                                                                                            \
-    }                                                                                              \
-  } while (0)
-
 bool pipe_supported(int dtype, int D, int G_T) {
   if (dtype == LOKI_DTYPE_BF16) return (D == 64 || D == 128 || (D == 256 && G_T <= 4)) && G_T <= 8;
   return (D == 64 || D == 128) && G_T <= 8;
 }
 
 int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big) {
-#define LOKI_OCC(T, GT, VEC, DT) (big ? occupancy_t<T, GT, VEC, DT, GT == 1>(smem) : occupancy_t<T, GT, VEC, DT, false>(smem))
-  LOKI_PIPE_DISPATCH(dtype, D, G_T, LOKI_OCC);
-#undef LOKI_OCC
+  if (dtype == LOKI_DTYPE_BF16) {
+    if (D == 64) return pipe_occ_bf16_64(G_T, smem, big);
+    if (D == 128) return pipe_occ_bf16_128(G_T, smem, big);
+    if (D == 256) return pipe_occ_bf16_256(G_T, smem, big);
+  } else {
+    if (D == 64) return pipe_occ_f32_64(G_T, smem, big);
+    if (D == 128) return pipe_occ_f32_128(G_T, smem, big);
+  }
   return 0;
 }
 
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
                         cudaStream_t st, bool big) {
-#define LOKI_LAUNCH(T, GT, VEC, DT)                                                   \
-  (big ? launch_pipe_t<T, GT, VEC, DT, GT == 1>(p, grid, smem, maps, st)              \
-       : launch_pipe_t<T, GT, VEC, DT, false>(p, grid, smem, maps, st))
-  LOKI_PIPE_DISPATCH(dtype, p.D, G_T, LOKI_LAUNCH);
-#undef LOKI_LAUNCH
+  if (dtype == LOKI_DTYPE_BF16) {
+    if (p.D == 64) return pipe_launch_bf16_64(p, G_T, grid, smem, maps, st, big);
+    if (p.D == 128) return pipe_launch_bf16_128(p, G_T, grid, smem, maps, st, big);
+    if (p.D == 256) return pipe_launch_bf16_256(p, G_T, grid, smem, maps, st, big);
+  } else {
+    if (p.D == 64) return pipe_launch_f32_64(p, G_T, grid, smem, maps, st, big);
+    if (p.D == 128) return pipe_launch_f32_128(p, G_T, grid, smem, maps, st, big);
+  }
   return cudaErrorInvalidValue;
 }
 
