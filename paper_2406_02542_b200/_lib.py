@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libloki_b200.so")
+LIB_PATH = os.environ.get("LOKI_LIB_PATH") or os.path.join(PKG_DIR, "libloki_b200.so")  # override: A/B tuning only
 
 LOKI_OK = 0
 LOKI_ERR_SHAPE = 1

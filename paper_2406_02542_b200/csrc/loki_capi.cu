@@ -279,13 +279,18 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   p.hbits = G_T <= 2 ? 11 : (G_T == 4 ? 10 : 9);
   const int d = a->d < 1 ? 1 : a->d;
   const int vec = pl->tg.vec;
-  p.split_k = !mma && env_int("LOKI_SPLITK", 1) != 0 && d < g.D && d % vec == 0 && ((g.D - d) * e) % 32 == 0;
+  // split-K: phase 3 skips the lead columns and adds the phase-1 partial score.  Tensor-core path: compiled
+  // for d = 32 of D = 128 (128 B + 64 B K pieces); the partial scores take Lc words of shared memory per
+  // head, so not with the 8192-row chunks
+  // (r01: no gain on the tensor-core path at C2, 210.5 vs 211.3 us, and 16 KB more smem: opt-in there)
+  p.split_k = env_int("LOKI_SPLITK", mma ? 0 : 1) != 0 && d < g.D &&
+              (mma ? (d == 32 && g.D == 128 && G_T <= 4) : (d % vec == 0 && ((g.D - d) * e) % 32 == 0));
   if (mma) p.r3 = 8;
   // one lane per lead row when the row is a TMA swizzle span (64 / 128 B) and r1 covers whole lanes
   const int lead_rb = p.dbox * e;
   // G == 1: one lane per lead row (r1 % 64); G >= 2 (bf16): tensor-core scores on 16-row blocks
   const bool lead_ok = (lead_rb == 64 || lead_rb == 128) && env_int("LOKI_LEAD_LPR", 1) != 0 &&
-                       (G_T == 1 ? p.r1 % 64 == 0 : (g.dtype == LOKI_DTYPE_BF16 && p.r1 % 16 == 0));
+                       (G_T == 1 ? p.r1 % (lead_rb == 64 ? 64 : 32) == 0 : (g.dtype == LOKI_DTYPE_BF16 && p.r1 % 16 == 0));
   p.lead_swz = lead_ok ? lead_rb : 0;
   if (g.dtype == LOKI_DTYPE_BF16 && G_T >= 2 && p.lead_swz == 0)  // bf16 groups need the tensor-core lead path
     return fail(LOKI_ERR_UNSUPPORTED, "pipe: bf16 query groups need 64 / 128 B lead rows (d = %d)", d);
@@ -293,6 +298,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // MHA at long sequences: 2x larger chunks (fewer per-item latency bubbles; r01: TGT 683 -> 658 us,
   // C2 213 -> 219 us, so only from 16K rows on)
   pl->big = G_T == 1 && env_int("LOKI_PIPE_BIG", a->S_max >= 16384 ? 1 : 0) != 0;
+  if (pl->big && mma) p.split_k = 0;
   const int nbg = pl->big ? 2 * loki::pipe_nb() : loki::pipe_nb();
   const int kNB = G_T >= nbg ? 1 : nbg / G_T;
   const int Lc = kNB * 128 * loki::pipe_warps();
@@ -385,7 +391,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   p.debug = env_int("LOKI_DEBUG", 0);
   p.trace = (loki::g_phase_trace != nullptr && p.n_tickets * 4 <= (long long)loki::g_phase_trace_ctas * 8)
                 ? loki::g_phase_trace : nullptr;
-  loki::TmaDesc maps[3];
+  loki::TmaDesc maps[4];
   if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, p.mma != 0, p.lead_swz, maps))
     return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
   cudaError_t e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big);

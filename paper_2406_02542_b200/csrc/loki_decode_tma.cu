@@ -358,7 +358,7 @@ bool encode4d(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_kv_g
 }
 
 bool encode_rows(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_kv_geom& g, int width = 0,
-                 bool swizzle128 = false) {
+                 int swizzle = 0, CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B) {
   const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   const CUtensorMapDataType dt =
       g.dtype == LOKI_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -367,8 +367,9 @@ bool encode_rows(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_k
   cuuint32_t box[2] = {(cuuint32_t)(width > 0 ? width : g.D), 1};
   cuuint32_t es[2] = {1, 1};
   return enc(reinterpret_cast<CUtensorMap*>(out->bytes), dt, 2, const_cast<void*>(base), dims, str, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
+             promo,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -392,9 +393,14 @@ bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int db
   const CUtensorMapSwizzle ls = lead_swz == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                : (lead_swz == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
   if (!encode4d(enc, &maps[0], K, g, dbox, r1, CU_TENSOR_MAP_L2_PROMOTION_L2_64B, ls)) return false;
-  if (mma)  // tensor-core phase 3: 128 B row halves, 128B-swizzled (conflict-free ldmatrix)
-    return encode_rows(enc, &maps[1], K, g, 64, true) && encode_rows(enc, &maps[2], V, g, 64, true);
-  return encode_rows(enc, &maps[1], K, g, g.D - kcol0) && encode_rows(enc, &maps[2], V, g);
+  if (mma) {  // tensor-core phase 3: 128 B row pieces 128B-swizzled, a trailing 64 B K piece 64B-swizzled
+    // split-K reads K from column d: 64 B promotion fetches exactly the sectors after the lead columns
+    const CUtensorMapL2promotion kp = kcol0 > 0 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    return encode_rows(enc, &maps[1], K, g, 64, 128, kp) && encode_rows(enc, &maps[2], V, g, 64, 128) &&
+           encode_rows(enc, &maps[3], K, g, 32, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_64B);
+  }
+  return encode_rows(enc, &maps[1], K, g, g.D - kcol0) && encode_rows(enc, &maps[2], V, g) &&
+         encode_rows(enc, &maps[3], K, g);
 }
 
 template <typename T, int G_T, int VEC, int D_T>

@@ -34,6 +34,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "loki_fused.cuh"
 #include "loki_tma.cuh"
 
@@ -604,14 +606,15 @@ __device__ __forceinline__ unsigned long long pk2(uint32_t lo, uint32_t hi) {
 // approx stores are coalesced.
 template <typename T, int RB>
 __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint8_t* tile, int rows_here,
-                                                 const unsigned long long (&q2)[32], uint32_t* keys0,
+                                                 const unsigned long long (&q2)[RB / (2 * sizeof(T))], uint32_t* keys0,
                                                  uint32_t* kl, float* approx0, uint32_t* hist, int hshift) {
   constexpr int NCH = RB / 16;
+  constexpr int RIF = RB == 64 ? 2 : 1;  // rows in flight per lane (register budget)
   const int lane = lane_id();
-  for (int r0 = 0; r0 < p.r1; r0 += 64) {
-    uint4 v[2][NCH];
+  for (int r0 = 0; r0 < p.r1; r0 += 32 * RIF) {
+    uint4 v[RIF][NCH];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < RIF; ++i) {
       const int rr = r0 + 32 * i + lane;
       const int sw = RB == 64 ? ((rr >> 1) & 3) : (rr & 7);
 #pragma unroll
@@ -619,7 +622,7 @@ __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint
         v[i][c] = *reinterpret_cast<const uint4*>(tile + rr * RB + ((c ^ sw) << 4));
     }
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < RIF; ++i) {
       unsigned long long acc = 0ull;
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
@@ -781,29 +784,32 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
     }
     if (consumed || (sizeof(T) == 2 && G_T >= 2)) {  // (bf16 groups always take the tensor-core path: host)
     } else if (G_T == 1 && p.lead_swz != 0) {  // one lane per row (swizzled lead rows)
-      constexpr int Q2 = 32;  // element pairs of the widest lead row (128 B of bf16)
-      unsigned long long q2[Q2];
+      // q as fp32 pairs, sized to the lead row so only the live half of a wider array is kept
+      auto run = [&](auto rbc) {
+        constexpr int RB = decltype(rbc)::value;
+        constexpr int Q2 = RB / (2 * E);
+        unsigned long long q2[Q2];
 #pragma unroll
-      for (int j = 0; j < Q2; ++j) {
-        const int c0 = 2 * j, c1 = 2 * j + 1;
-        const float a = c0 < p.d ? p.q_hat[qrow0 * p.D + c0] : 0.f;
-        const float bq = c1 < p.d ? p.q_hat[qrow0 * p.D + c1] : 0.f;
-        q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
-      }
-      for (int k = 0; k < mine; ++k, rp.advance(1)) {
-        mbar_wait(&wbar[rp.slot], rp.phase);
-        const uint8_t* tile = wring + rp.slot * SB;
-        const int i = w + k * kPW;
-        const int rows_here = min(R1, n - i * R1);
-        uint32_t* k0 = keys_u + i * R1;
-        float* a0 = approx_u ? approx_u + i * R1 : nullptr;
-        if (p.lead_swz == 64)
-          lead_consume_lpr<T, 64>(p, tile, rows_here, q2, k0, kl0(i), a0, hist, hshift);
-        else
-          lead_consume_lpr<T, 128>(p, tile, rows_here, q2, k0, kl0(i), a0, hist, hshift);
-        __syncwarp();
-        if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
-      }
+        for (int j = 0; j < Q2; ++j) {
+          const int c0 = 2 * j, c1 = 2 * j + 1;
+          const float a = c0 < p.d ? p.q_hat[qrow0 * p.D + c0] : 0.f;
+          const float bq = c1 < p.d ? p.q_hat[qrow0 * p.D + c1] : 0.f;
+          q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
+        }
+        for (int k = 0; k < mine; ++k, rp.advance(1)) {
+          mbar_wait(&wbar[rp.slot], rp.phase);
+          const uint8_t* tile = wring + rp.slot * SB;
+          const int i = w + k * kPW;
+          const int rows_here = min(R1, n - i * R1);
+          uint32_t* k0 = keys_u + i * R1;
+          float* a0 = approx_u ? approx_u + i * R1 : nullptr;
+          lead_consume_lpr<T, RB>(p, tile, rows_here, q2, k0, kl0(i), a0, hist, hshift);
+          __syncwarp();
+          if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+        }
+      };
+      if (p.lead_swz == 64) run(std::integral_constant<int, 64>{});
+      else run(std::integral_constant<int, 128>{});
     } else if constexpr (!(sizeof(T) == 2 && G_T >= 2))
     for (int k = 0; k < mine; ++k, rp.advance(1)) {
       mbar_wait(&wbar[rp.slot], rp.phase);
@@ -1085,29 +1091,38 @@ __device__ void stream_B_simt(const PipeParams& p, const CUtensorMap* krow_map, 
 
 // Phase 3 on the tensor cores (bf16 caches).  A stage is 8 gathered rows
 // (4 KB at D = 128: many small stages keep 16 warps per SM issuing gathers,
-// tools/gatherbench.cu): K and V as 128 B row halves, 128B-swizzled by TMA so
-// ldmatrix is conflict-free.  Per stage, with the 8 rows as M rows 0..7 of
-// m16n8k16 (rows 8..15 zero):  S^T[8 x 8] = K[8 x D] . Qc[D x 8]  and
-// O^T[D x 8] += V^T[D x 8] . P^T[8 x 8]  (fp32 accumulate).  Columns carry
-// (head, hi / lo part): q * qscale and the softmax weights are split into two
-// bf16 terms, so both products keep ~2^-17 relative accuracy.
-// G <= 4: column 2h + part;  G == 8: columns = heads, hi and lo in two mmas.
-template <int G_T, int D_T>
-__device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u,
-                             int n, int row_base, size_t qrow0, const uint32_t* ents, uint8_t* wring, uint64_t* wbar,
-                             RingPos& rp, float* wpart) {
-  constexpr int NH = D_T / 64;             // 128 B row halves
-  constexpr int KS = D_T / 16;             // k-steps of q.K == m-tiles of P.V
+// tools/gatherbench.cu), 128B/64B-swizzled by TMA so ldmatrix is conflict-free:
+//   V   as 128 B row halves (NH x 1 KB), then
+//   K   columns [kc0, D): `ka` 128 B pieces (1 KB each) + `kb` 64 B piece (512 B).
+// kc0 = 0, or d with split-K: the phase-1 partial score q[:d].K[:d] (from the
+// keys) is added to the logit and the leading d columns are not fetched again.
+// Per stage, with the 8 rows as M rows 0..7 of m16n8k16 (rows 8..15 zero):
+//   S^T[8 x 8] = K[8 x D'] . Qc[D' x 8]  and  O^T[D x 8] += V^T[D x 8] . P^T[8 x 8]
+// (fp32 accumulate).  Columns carry (head, hi / lo part): q * qscale and the
+// softmax weights are split into two bf16 terms, so both products keep ~2^-17
+// relative accuracy.  G <= 4: column 2h + part;  G == 8: columns = heads, hi
+// and lo in two mmas.
+template <int G_T, int D_T, int KC0>
+__device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map,
+                             const CUtensorMap* krow64_map, int u, int n, int row_base, size_t qrow0,
+                             const uint32_t* ents, const float* apx, uint8_t* wring, uint64_t* wbar, RingPos& rp,
+                             float* wpart) {
+  constexpr int NH = D_T / 64;             // 128 B row halves of V
+  constexpr int KS = D_T / 16;             // max k-steps of q.K == m-tiles of P.V
   constexpr int R = 8;                     // rows per stage
-  constexpr int HW = R * 128;              // bytes of one half block (one swizzle atom)
+  constexpr int HW = R * 128;              // bytes of one 128 B-row block (one swizzle atom)
   constexpr int NHL = G_T == 8 ? 2 : 1;    // heads per lane
   constexpr bool kSplitCols = G_T < 8;
   const int lane = lane_id(), w = warp_id();
   const int G = p.G;
   const int nsw = p.nst, SB = p.stage_bytes;
   const int g8 = lane >> 2, t4 = lane & 3;
+  constexpr bool split = KC0 > 0;
+  constexpr int kc0 = KC0;                 // first gathered K column (compile time: keeps the loops static)
+  constexpr int ka = (D_T - kc0) / 64, kbp = ((D_T - kc0) % 64) / 32;  // K pieces: 128 B and 64 B
+  constexpr int KSK = (D_T - kc0) / 16;    // k-steps of q.K over the gathered columns
   const int nstage = ceil_div(n, R);
-  const unsigned stage_bytes = (unsigned)(R * D_T * 2 * 2);
+  const unsigned stage_bytes = (unsigned)(R * (D_T + (D_T - kc0)) * 2);
   const bool want_logits = p.weights_out != nullptr;
   const int mine = nstage > w ? ceil_div(nstage - w, kPW) : 0;  // stages w, w + kPW, ...
   auto issue = [&](int k, const RingPos& at) {
@@ -1125,10 +1140,13 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
       const int a3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
       if (lane == 0) {
 #pragma unroll
-        for (int h = 0; h < NH; ++h) {
-          tma_gather4(dst + h * HW + qq * 512, krow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
-          tma_gather4(dst + (NH + h) * HW + qq * 512, vrow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
-        }
+        for (int h = 0; h < NH; ++h)
+          tma_gather4(dst + h * HW + qq * 512, vrow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
+#pragma unroll
+        for (int j = 0; j < ka; ++j)
+          tma_gather4(dst + (NH + j) * HW + qq * 512, krow_map, kc0 + 64 * j, a0, a1, a2, a3, &wbar[at.slot]);
+        if constexpr (kbp > 0)
+          tma_gather4(dst + (NH + ka) * HW + qq * 256, krow64_map, D_T - 32, a0, a1, a2, a3, &wbar[at.slot]);
       }
     }
   };
@@ -1140,13 +1158,13 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
   uint32_t qb[KS][2], ql[G_T == 8 ? KS : 1][2];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
-    const int k0 = 16 * ks + 2 * t4;
+    const int k0 = kc0 + 16 * ks + 2 * t4;
     const int head = kSplitCols ? (g8 >> 1) : g8;
     float v[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int dim = k0 + (i & 1) + (i >> 1) * 8;
-      v[i] = head < G ? p.q_hat[(qrow0 + head) * D_T + dim] * p.qscale : 0.f;
+      v[i] = (head < G && ks < KSK) ? p.q_hat[(qrow0 + head) * D_T + dim] * p.qscale : 0.f;
     }
     if (kSplitCols) {
       const bool lo = g8 & 1;
@@ -1181,13 +1199,23 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
     float S[4] = {0.f, 0.f, 0.f, 0.f}, S2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      uint32_t a2[2];
-      asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
-                   : "=r"(a2[0]), "=r"(a2[1])
-                   : "r"(swz128(sb + (ks >> 2) * HW, rX, ((ks & 3) << 1) | cX)));
-      const uint32_t a[4] = {a2[0], 0u, a2[1], 0u};
-      mma_bf16(S, a, qb[ks][0], qb[ks][1]);
-      if (!kSplitCols) mma_bf16(S2, a, ql[ks][0], ql[ks][1]);
+      if constexpr (true) {
+        if (ks >= KSK) continue;
+        uint32_t addr;
+        if (ks < 4 * ka) {  // 128 B piece ks / 4
+          addr = swz128(sb + (NH + (ks >> 2)) * HW, rX, ((ks & 3) << 1) | cX);
+        } else {            // trailing 64 B piece (64B swizzle: chunk ^ (row >> 1 & 3))
+          const int c = ((ks - 4 * ka) << 1) | cX;
+          addr = sb + (NH + ka) * HW + rX * 64 + ((c ^ ((rX >> 1) & 3)) << 4);
+        }
+        uint32_t a2[2];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];"
+                     : "=r"(a2[0]), "=r"(a2[1])
+                     : "r"(addr));
+        const uint32_t a[4] = {a2[0], 0u, a2[1], 0u};
+        mma_bf16(S, a, qb[ks][0], qb[ks][1]);
+        if (!kSplitCols) mma_bf16(S2, a, ql[ks][0], ql[ks][1]);
+      }
     }
     const int tA = st * R + g8;
     const uint32_t eA = tA < n ? ents[tA] : 0u;
@@ -1197,6 +1225,7 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
       const int head = kSplitCols ? t4 : 2 * t4 + j;
       x[j] = kSplitCols ? S[0] + S[1] : S[j] + S2[j];
       const bool ok = head < G && ((eA >> (24 + head)) & 1u);
+      if (split && ok) x[j] += apx[head * p.Lc + tA];  // phase-1 partial over the first d columns
       float tm = ok ? x[j] : -CUDART_INF_F;
       tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
       tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
@@ -1243,7 +1272,7 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
       uint32_t a2[2];
       asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
                    : "=r"(a2[0]), "=r"(a2[1])
-                   : "r"(swz128(sb + (NH + (dim >> 6)) * HW, rX, (dim & 63) >> 3)));
+                   : "r"(swz128(sb + (dim >> 6) * HW, rX, (dim & 63) >> 3)));
       const uint32_t a[4] = {a2[0], a2[1], 0u, 0u};
       mma_bf16(O[mt], a, pb, 0u);
       if (!kSplitCols) mma_bf16(O[mt], a, pl, 0u);
@@ -1283,8 +1312,8 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
 
 // B(u, q): rows [q * Lc, (q + 1) * Lc).  kNB 128-row blocks per warp.
 template <typename T, int G_T, int VEC, int D_T, bool BIG>
-__device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map, int u, int q,
-                      int half, uint8_t* ring, uint8_t* wring, uint64_t* wbar, uint32_t* ents, RingPos& rp,
+__device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CUtensorMap* vrow_map,
+                      const CUtensorMap* krow64_map, int u, int q, int half, uint8_t* ring, uint8_t* wring, uint64_t* wbar, uint32_t* ents, RingPos& rp,
                       PipeShared& sh) {
   constexpr int E = sizeof(T);
   constexpr int LPR3 = D_T / VEC;  // lanes per V row
@@ -1431,8 +1460,19 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   const int ldp = D + 2;
   float* wpart = reinterpret_cast<float*>(ring);  // [kPW][G_T][D + 2]; every ring slot has been consumed
   const int row_base = (int)(((long long)b * p.Hkv + hk) * p.unit_rows);
-  if constexpr (sizeof(T) == 2)  // bf16: always the tensor-core phase 3 (host sets p.mma)
-    stream_B_mma<G_T, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, wring, wbar, rp, wpart);
+  if constexpr (sizeof(T) == 2) {  // bf16: always the tensor-core phase 3 (host sets p.mma)
+    if constexpr (D_T == 128 && G_T <= 4) {
+      if (p.split_k)  // host: split-K on the tensor-core path means d == 32
+        stream_B_mma<G_T, D_T, 32>(p, krow_map, vrow_map, krow64_map, u, n, row_base, qrow0, ents, apx, wring, wbar,
+                                   rp, wpart);
+      else
+        stream_B_mma<G_T, D_T, 0>(p, krow_map, vrow_map, krow64_map, u, n, row_base, qrow0, ents, apx, wring, wbar,
+                                  rp, wpart);
+    } else {
+      stream_B_mma<G_T, D_T, 0>(p, krow_map, vrow_map, krow64_map, u, n, row_base, qrow0, ents, apx, wring, wbar, rp,
+                                wpart);
+    }
+  }
   else
     stream_B_simt<T, G_T, VEC, D_T>(p, krow_map, vrow_map, u, n, row_base, qrow0, ents, apx, wring, wbar, rp, wpart);
   __syncthreads();
@@ -1468,7 +1508,8 @@ template <typename T, int G_T, int VEC, int D_T, bool BIG>
 __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
                                                           const __grid_constant__ CUtensorMap lead_map,
                                                           const __grid_constant__ CUtensorMap krow_map,
-                                                          const __grid_constant__ CUtensorMap vrow_map) {
+                                                          const __grid_constant__ CUtensorMap vrow_map,
+                                                          const __grid_constant__ CUtensorMap krow64_map) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ PipeShared sh;
   // 1024 B alignment: the tensor-core path reads 128B-swizzled TMA tiles
@@ -1494,6 +1535,7 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
     prefetch_desc(&lead_map);
     prefetch_desc(&krow_map);
     prefetch_desc(&vrow_map);
+    prefetch_desc(&krow64_map);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended rows are visible
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1516,12 +1558,12 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
     const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
     int kind = 0;
     if (slot >= p.units) {  // tail slot: no A items left, all 2 nA tickets are half-size B items
-      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
+      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
                                       rp, sh);
     } else if (r < p.nA) {
       kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, sbar, sphase, rp, sh);
     } else if (slot >= p.lag) {
-      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
+      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
                                       rp, sh);
     }
     fence_proxy_async();  // this item's generic shared-memory writes precede the next item's TMA writes
@@ -1561,7 +1603,7 @@ inline cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, con
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const CUtensorMap* m = reinterpret_cast<const CUtensorMap*>(maps);
-  return cudaLaunchKernelEx(&cfg, kern, p, m[0], m[1], m[2]);
+  return cudaLaunchKernelEx(&cfg, kern, p, m[0], m[1], m[2], m[3]);
 }
 
 template <typename T, int G_T, int VEC, int D_T, bool BIG>
