@@ -212,7 +212,13 @@ class Workload:
         torch.cuda.synchronize()
         log(f"[bench] rank {rank}: built {L} layers of KV cache "
             f"({2 * L * B * self.Hkv_l * S * D * 2 / 1e9:.1f} GB bf16) in {time.time() - t0:.1f}s")
-        self.q_raw = torch.randn(L, B, self.Hq_l, D, device=dev, generator=gen)
+        if cfg.get("gqa_queries") == "correlated" and self.G > 1:
+            # group-correlated queries q_g = q_0 + 0.5 eps_g
+            q0 = torch.randn(L, B, self.Hkv_l, 1, D, device=dev, generator=gen)
+            eps = torch.randn(L, B, self.Hkv_l, self.G, D, device=dev, generator=gen)
+            self.q_raw = (q0 + 0.5 * eps).reshape(L, B, self.Hq_l, D).contiguous()
+        else:
+            self.q_raw = torch.randn(L, B, self.Hq_l, D, device=dev, generator=gen)
         self.k_raw = torch.randn(L, B, self.Hkv_l, D, device=dev, generator=gen)
         self.v_new = torch.randn(L, B, self.Hkv_l, D, device=dev, generator=gen)
         self.rows = torch.full((B,), S - 1, dtype=torch.int32, device=dev)
@@ -450,13 +456,26 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def union_rows(wl, dec):
+    """Mean |union over the query group of the selected rows| per (b, kv head) unit of one layer."""
+    import torch
+
+    import paper_2406_02542_b200 as L
+
+    _, diag = L.loki_decode(dec.q_hat, wl.K[0], wl.V[0], wl.lens, d=wl.d, k=wl.k, diagnostics=True)
+    idx = diag.indices.view(wl.B, wl.Hkv_l, wl.G * wl.k)
+    sizes = [torch.unique(idx[b, h]).numel() for b in range(wl.B) for h in range(wl.Hkv_l)]
+    return float(sum(sizes)) / len(sizes)
+
+
 def config_block(cfg, args, world, d, k):
     return {"workload": f"{args.config}: {cfg['desc']}", "layers": cfg["layers"], "global_batch": cfg["B"],
             "seq_len": cfg["S"], "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"], "head_dim": cfg["D"],
             "k_f": cfg["k_f"], "d_f": cfg["d_f"], "d": d, "k": k, "cache_dtype": "bf16",
             "rotary": f"pre-rotary PCA, rotate-then-project, base {cfg['base']:g}",
             "l2": "inputs larger than L2 (KV per layer >> 126 MB); no flush",
-            "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU"}
+            "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+            **({"gqa_queries": cfg.get("gqa_queries", "independent")} if cfg["Hq"] > cfg["Hkv"] else {})}
 
 
 # ----------------------------------------------------------------------------- main
@@ -472,9 +491,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the SDPA / flashinfer dense comparators")
+    ap.add_argument("--gqa-queries", default="independent", choices=["independent", "correlated"],
+                    help="GQA query heads: independent N(0,1), or q_0 + 0.5 eps per group (SURVEY 8(d) M2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config], gqa_queries=args.gqa_queries)
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, cfg, int(os.environ.get("WORLD_SIZE", "1")), rank)
@@ -519,7 +540,10 @@ def main():
 
     units = wl.B * wl.Hkv_l
     elem = 2
-    algo_bytes = metrics.loki_bytes(units, wl.S, wl.D, wl.d, wl.k, elem)  # U = k (MHA); GQA: union, see DESIGN
+    U = float(wl.k)
+    if wl.G > 1:  # GQA: rows gathered = |union of the group's selections|, measured on layer 0
+        U = union_rows(wl, decs[0])
+    algo_bytes = metrics.loki_bytes(units, wl.S, wl.D, wl.d, U, elem)
     dense_bytes = metrics.dense_bytes(units, wl.S, wl.D, elem)
     peaks = {}
     try:
@@ -594,6 +618,7 @@ def main():
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "pipe_decode_kernel (persistent; approx scores + top-k + tensor-core sparse attention)",
                          "algorithmic_bytes_per_launch": int(algo_bytes), "peak_source": peak_src,
+                         "rows_gathered_per_unit": round(U, 1),
                          "dense_achieved_gbs": round(dense_bytes / (dense_attn_us * 1e-6) / 1e9, 1)},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -299,15 +299,19 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // C2 213 -> 219 us, so only from 16K rows on)
   pl->big = G_T == 1 && env_int("LOKI_PIPE_BIG", a->S_max >= 16384 ? 1 : 0) != 0;
   if (pl->big && mma) p.split_k = 0;
-  const int nbg = pl->big ? 2 * loki::pipe_nb() : loki::pipe_nb();
-  const int kNB = G_T >= nbg ? 1 : nbg / G_T;
+  const int kNB = loki::pipe_blocks_per_warp(G_T, pl->big);
   const int Lc = kNB * 128 * loki::pipe_warps();
   if (Lc % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", Lc, p.r1);
   p.Lc = Lc;
   p.nA = loki::ceil_div(a->S_max, Lc);
+  // A chunks of >= 4096 rows: small GQA parts would make phase-1 items overhead-bound
+  p.La = env_int("LOKI_PIPE_LA", Lc >= 4096 ? Lc : 4096);
+  if (p.La < Lc) p.La = Lc;
+  if (p.La % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", p.La, p.r1);
+  p.nAa = loki::ceil_div(a->S_max, p.La);
   p.units = units;
   // speculative boundary-bin candidates (ranking-free path only: idx_out needs per-part counts)
-  p.spec = env_int("LOKI_SPEC", 0) != 0 && G_T <= 4 && a->idx_out == nullptr;  // opt-in: r01 measured a net loss
+  p.spec = env_int("LOKI_SPEC", 0) != 0 && G_T <= 4 && a->idx_out == nullptr && p.La == p.Lc;  // opt-in (net loss)
   p.ccap = a->S_max / 4 > 2048 ? a->S_max / 4 : 2048;
   pl->smem = loki::pipe_layout(G_T, &p);
   const size_t ring = (size_t)loki::pipe_warps() * p.nst * p.stage_bytes;
@@ -320,9 +324,10 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
   // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn
   const double lagx = env_int("LOKI_PIPE_LAG_X10", 40 * G) / 10.0;
-  int lag = (int)ceil(lagx * pl->grid / (double)(2 * p.nA));
+  const int per_slot = (p.nAa + p.nA) > 2 * p.nA ? (p.nAa + p.nA) : 2 * p.nA;
+  int lag = (int)ceil(lagx * pl->grid / (double)(p.nAa + p.nA));
   p.lag = lag < 1 ? 1 : (lag > units ? units : lag);
-  p.n_tickets = (long long)(units + p.lag) * (2 * p.nA);
+  p.n_tickets = (long long)(units + p.lag) * per_slot;
   // workspace: ctrl | hist | keys | sel | part | logits
   const int HB = 1 << p.hbits;
   size_t off = loki::align_up((size_t)(2 + 4 * (size_t)units) * 4, 256);

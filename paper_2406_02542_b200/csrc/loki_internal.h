@@ -69,7 +69,8 @@ struct PipeParams {
   int nst, stage_bytes, off_ring, off_bars, off_hist, off_ents;
   int r1, dbox, r3;
   long long unit_rows;
-  int units, Lc, nA, lag, hbits, cand_cap;
+  int units, Lc, nA, lag, hbits, cand_cap;  // Lc / nA: B-part rows / B parts per unit
+  int La, nAa;       // A-chunk rows / A chunks per unit (La >= Lc: phase-1 items are not overhead-bound)
   long long n_tickets;
   int split_k;       // 1: phase 3 gathers K columns [d, D) only and reuses the phase-1 partial score
   int mma;           // 1: tensor-core phase 3 (bf16 caches): 8-row stages of 128B-swizzled row halves
@@ -156,5 +157,9 @@ cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_
 int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big);
 int pipe_warps();
 int pipe_nb();
+// 128-row blocks per warp in a B part (Lc = blocks * 128 * warps), shared by kernel and host
+__host__ __device__ constexpr int pipe_blocks_per_warp(int G_T, bool big) {
+  return G_T == 1 ? (big ? 8 : 4) : (G_T == 8 ? 1 : 2);
+}
 
 }  // namespace loki

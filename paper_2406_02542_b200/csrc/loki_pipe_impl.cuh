@@ -306,7 +306,7 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
   unsigned long long* candC = candB + cap;
   const int Lh = p.Lc / 2;                      // idx_out offsets at half-part granularity
   const int nhp = ceil_div(S > 0 ? S : 1, Lh);
-  const int nparts_a = ceil_div(S > 0 ? S : 1, p.Lc);
+  const int nparts_a = ceil_div(S > 0 ? S : 1, p.La);
   for (int g = 0; g < G; ++g) {
     const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
     uint32_t* gh = p.hist + ((size_t)u * G + g) * HB;
@@ -706,10 +706,10 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
   const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G;
   int S = p.lens[b];
   S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
-  const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
+  const int nparts = ceil_div(S > 0 ? S : 1, p.La);
   if (c >= nparts) return 0;  // past this unit's length: not an arrival
-  const int row0 = c * p.Lc;
-  const int n = max(0, min(S - row0, p.Lc));
+  const int row0 = c * p.La;
+  const int n = max(0, min(S - row0, p.La));
   const int HB = 1 << p.hbits, hshift = 32 - p.hbits;
   for (int i = tid; i < G * HB; i += kPT) hist[i] = 0u;
   __syncthreads();
@@ -1319,8 +1319,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   constexpr int LPR3 = D_T / VEC;  // lanes per V row
   constexpr int RPW3 = 32 / LPR3;
   constexpr int ROWB = D_T * E;
-  constexpr int NBG = BIG ? 2 * LOKI_PIPE_NB : LOKI_PIPE_NB;  // 128-row blocks per warp at G = 1
-  constexpr int kNB = G_T >= NBG ? 1 : NBG / G_T;  // Lc == kNB * 128 * kPW (host)
+  constexpr int kNB = pipe_blocks_per_warp(G_T, BIG);  // Lc == kNB * 128 * kPW (host)
   const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int nsw = p.nst, SB = p.stage_bytes;
   const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G, D = D_T;
@@ -1542,7 +1541,8 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
   if (tid == 0) sh.next_ticket = atomicAdd(&p.ctrl[0], 1u);
   __syncthreads();
   RingPos rp(nsw);
-  const int per_slot = 2 * p.nA;  // A(u, 0..nA-1) then B(u - lag, 0..nA-1); tail slots: half B items
+  // slot = A(u, 0..nAa-1), B(u - lag, 0..nA-1); tail slots (no A left): 2 nA half-size B items
+  const int per_slot = max(p.nAa + p.nA, 2 * p.nA);
   for (;;) {
     const unsigned t = sh.next_ticket;
     __syncthreads();
@@ -1557,13 +1557,14 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
     const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
     const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
     int kind = 0;
-    if (slot >= p.units) {  // tail slot: no A items left, all 2 nA tickets are half-size B items
-      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
+    if (slot >= p.units) {  // tail slot: no A items left, half-size B items
+      if (r < 2 * p.nA)
+        kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
                                       rp, sh);
-    } else if (r < p.nA) {
+    } else if (r < p.nAa) {
       kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, sbar, sphase, rp, sh);
-    } else if (slot >= p.lag) {
-      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r - p.nA, -1, ring, wring, wbar, ents,
+    } else if (slot >= p.lag && r < p.nAa + p.nA) {
+      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r - p.nAa, -1, ring, wring, wbar, ents,
                                       rp, sh);
     }
     fence_proxy_async();  // this item's generic shared-memory writes precede the next item's TMA writes
