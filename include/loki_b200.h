@@ -165,6 +165,16 @@ loki_status loki_rope(const void* x, void* out, int32_t io_dtype, int64_t n_rows
 loki_status loki_index_status(const int64_t* idx, int32_t n, int64_t bound, int32_t* status,
                               void* stream);
 
+/* Batched PCA transform (the k @ P / q @ P products of attention.py:201-202
+ * and transform_step's projection, attention.py:316-341, for whole blocks):
+ *   out[b, h, s, :] = x[b, h, s, :] . P[h / G]
+ * x, out: [B, H, S, D] with element strides {b, h, s} (D contiguous), dtype
+ * f32 or bf16 each; P [H / G, D, D] fp32 row-major (calibration.py:117-123).
+ * fp32 accumulation in index order.  D <= 128. */
+loki_status loki_project_rows(const void* x, int32_t x_dtype, const int64_t* x_strides, const float* P,
+                              void* out, int32_t out_dtype, const int64_t* out_strides, int32_t B, int32_t H,
+                              int32_t S, int32_t D, int32_t G, void* stream);
+
 /* Diagnostics: subsequent TMA-path loki_decode launches whose grid fits in
  * max_ctas record eight %globaltimer stamps per CTA into buf [max_ctas][8]
  * (start, phase 1 done, radix passes done, tie counts exchanged, selection

@@ -42,7 +42,7 @@ EXPORTED = (
     "loki_last_error", "loki_abi_version", "loki_device_check", "loki_decode",
     "loki_decode_workspace_bytes", "loki_decode_plan", "loki_append_kv",
     "loki_gathered_scores", "loki_weighted_sum", "loki_weighted_sum_workspace",
-    "loki_softmax_rows", "loki_rope", "loki_index_status", "loki_set_phase_trace",
+    "loki_softmax_rows", "loki_rope", "loki_index_status", "loki_set_phase_trace", "loki_project_rows",
 )
 
 
@@ -86,6 +86,7 @@ _SIGS = {
     "loki_rope": (_I32, [_P, _P, _I32, _I64, _I32, _P, _P, _P]),
     "loki_index_status": (_I32, [_P, _I32, _I64, _P, _P]),
     "loki_set_phase_trace": (_I32, [_P, _I32]),
+    "loki_project_rows": (_I32, [_P, _I32, _P, _P, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _P]),
 }
 
 _lock = threading.Lock()

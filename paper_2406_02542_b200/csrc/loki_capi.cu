@@ -595,6 +595,22 @@ loki_status loki_set_phase_trace(int64_t* buf, int32_t max_ctas) {
   return LOKI_OK;
 }
 
+loki_status loki_project_rows(const void* x, int32_t x_dtype, const int64_t* x_strides, const float* P,
+                              void* out, int32_t out_dtype, const int64_t* out_strides, int32_t B, int32_t H,
+                              int32_t S, int32_t D, int32_t G, void* stream) {
+  if (B < 0 || H < 1 || S < 0 || D < 1 || G < 1 || H % G != 0)
+    return fail(LOKI_ERR_SHAPE, "invalid projection shape B=%d H=%d S=%d D=%d G=%d", B, H, S, D, G);
+  if (D > 128) return fail(LOKI_ERR_UNSUPPORTED, "projection head dim %d > 128", D);
+  if ((x_dtype != LOKI_DTYPE_F32 && x_dtype != LOKI_DTYPE_BF16) ||
+      (out_dtype != LOKI_DTYPE_F32 && out_dtype != LOKI_DTYPE_BF16))
+    return fail(LOKI_ERR_UNSUPPORTED, "projection dtypes %d -> %d", x_dtype, out_dtype);
+  if (x == nullptr || P == nullptr || out == nullptr || x_strides == nullptr || out_strides == nullptr)
+    return fail(LOKI_ERR_SHAPE, "null projection argument");
+  cudaError_t e = loki::launch_project_rows(x, x_dtype, P, out, out_dtype, B, H, S, D, G, x_strides, out_strides,
+                                            static_cast<cudaStream_t>(stream));
+  return cuda_status(e, "loki_project_rows launch");
+}
+
 loki_status loki_index_status(const int64_t* idx, int32_t n, int64_t bound, int32_t* status, void* stream) {
   if (n < 0 || status == nullptr) return fail(LOKI_ERR_SHAPE, "invalid index-status arguments");
   cudaError_t e = loki::launch_index_status(idx, n, bound, status, static_cast<cudaStream_t>(stream));

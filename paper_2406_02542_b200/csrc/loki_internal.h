@@ -144,6 +144,8 @@ cudaError_t launch_softmax_rows(const float* x, int64_t rows, int n, int64_t str
 cudaError_t launch_rope(const void* x, void* out, int io_dtype, int64_t n_rows, int D,
                         const int64_t* positions, const double* inv_freq, cudaStream_t st);
 cudaError_t launch_index_status(const int64_t* idx, int n, int64_t bound, int32_t* status, cudaStream_t st);
+cudaError_t launch_project_rows(const void* x, int x_dtype, const float* P, void* out, int out_dtype, int B, int H,
+                                int S, int D, int G, const int64_t* xs, const int64_t* os, cudaStream_t st);
 
 // persistent pipelined decode (loki_pipe.cu)
 size_t pipe_layout(int G_T, PipeParams* p);

@@ -180,3 +180,62 @@ cudaError_t launch_index_status(const int64_t* idx, int n, int64_t bound, int32_
 }
 
 }  // namespace loki
+
+// ---------------------------------------------------------------- row projection
+// out[b, h, s, :] = x[b, h, s, :] . P[h / G]  (fp32 accumulate in index order):
+// the PCA transform of whole caches / query blocks (the batched form of the
+// k @ P / q @ P products of attention.py:201-202, e.g. for a prefill or an
+// HF cache update).  One CTA per (b, h, 32-row block); P[h / G] staged in
+// shared memory; I/O dtype f32 or bf16.
+namespace loki {
+namespace {
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(128) project_rows_kernel(const TI* __restrict__ x, const float* __restrict__ P,
+                                                          TO* __restrict__ out, int H, int S, int D, int G,
+                                                          int64_t x_sb, int64_t x_sh, int64_t x_ss, int64_t o_sb,
+                                                          int64_t o_sh, int64_t o_ss) {
+  extern __shared__ float ps[];  // [D][D] then [32][D] rows
+  const int bh = blockIdx.x, b = bh / H, h = bh % H;
+  const int s0 = blockIdx.y * 32;
+  const float* Ph = P + (size_t)(h / G) * D * D;
+  float* xs = ps + (size_t)D * D;
+  for (int i = threadIdx.x; i < D * D; i += blockDim.x) ps[i] = Ph[i];
+  const int rows = min(32, S - s0);
+  for (int i = threadIdx.x; i < rows * D; i += blockDim.x) {
+    const int r = i / D, c = i % D;
+    xs[i] = Elem<TI>::to_f(x[b * x_sb + h * x_sh + (int64_t)(s0 + r) * x_ss + c]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < rows * D; i += blockDim.x) {
+    const int r = i / D, c = i % D;
+    float acc = 0.f;
+    for (int t = 0; t < D; ++t) acc = fmaf(xs[r * D + t], ps[t * D + c], acc);
+    out[b * o_sb + h * o_sh + (int64_t)(s0 + r) * o_ss + c] = Elem<TO>::from_f(acc);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_project_rows(const void* x, int x_dtype, const float* P, void* out, int out_dtype, int B, int H,
+                                int S, int D, int G, const int64_t* xs, const int64_t* os, cudaStream_t st) {
+  if (B == 0 || S == 0) return cudaSuccess;
+  const size_t smem = (size_t)(D * D + 32 * D) * sizeof(float);
+  dim3 grid((unsigned)(B * H), (unsigned)ceil_div(S, 32));
+#define LOKI_PR(TI, TO)                                                                                      \
+  do {                                                                                                       \
+    auto k = project_rows_kernel<TI, TO>;                                                                    \
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    if (e != cudaSuccess) return e;                                                                          \
+    k<<<grid, 128, smem, st>>>(static_cast<const TI*>(x), P, static_cast<TO*>(out), H, S, D, G, xs[0], xs[1], \
+                               xs[2], os[0], os[1], os[2]);                                                  \
+    return cudaGetLastError();                                                                               \
+  } while (0)
+  if (x_dtype == LOKI_DTYPE_BF16 && out_dtype == LOKI_DTYPE_BF16) LOKI_PR(__nv_bfloat16, __nv_bfloat16);
+  if (x_dtype == LOKI_DTYPE_BF16 && out_dtype == LOKI_DTYPE_F32) LOKI_PR(__nv_bfloat16, float);
+  if (x_dtype == LOKI_DTYPE_F32 && out_dtype == LOKI_DTYPE_BF16) LOKI_PR(float, __nv_bfloat16);
+  LOKI_PR(float, float);
+#undef LOKI_PR
+}
+
+}  // namespace loki
