@@ -158,7 +158,6 @@ cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_
                         cudaStream_t st, bool big);
 int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big);
 int pipe_warps();
-int pipe_nb();
 // 128-row blocks per warp in a B part (Lc = blocks * 128 * warps), shared by kernel and host
 __host__ __device__ constexpr int pipe_blocks_per_warp(int G_T, bool big) {
   return G_T == 1 ? (big ? 8 : 4) : (G_T == 8 ? 1 : 2);

@@ -18,7 +18,6 @@ int pipe_occ_f32_128(int, size_t, bool);
 
 
 int pipe_warps() { return kPW; }
-int pipe_nb() { return LOKI_PIPE_NB; }
 
 size_t pipe_layout(int G_T, PipeParams* p) {
   size_t off = 0;

@@ -47,9 +47,6 @@ using namespace tma;
 using fused::kMaxG;
 using fused::merge_state;
 
-#ifndef LOKI_PIPE_NB
-#define LOKI_PIPE_NB 4  // 128-row blocks per warp in a G = 1 chunk (Lc = NB * 128 * warps)
-#endif
 #ifndef LOKI_PIPE_WARPS
 #define LOKI_PIPE_WARPS 8
 #endif
@@ -195,21 +192,6 @@ __device__ __forceinline__ uint32_t u4_at(const uint4& v, int e) {
   return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
 }
 
-// f(jb, kk): lane's rows jb..jb+3 (caller masks rows >= rb); warp-uniform calls.
-template <typename F>
-__device__ __forceinline__ void scan_rows(const uint32_t* keys, int ra, int rb, F&& f) {
-  const int lane = lane_id();
-  for (int j0 = ra; j0 < rb; j0 += 128 * kSU) {
-    uint4 kk[kSU];
-#pragma unroll
-    for (int u = 0; u < kSU; ++u) {
-      const int jb = j0 + 128 * u + 4 * lane;
-      kk[u] = jb < rb ? ld_keys4(keys, jb) : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int u = 0; u < kSU; ++u) f(j0 + 128 * u + 4 * lane, kk[u]);
-  }
-}
 
 __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
   const int lane = lane_id();
