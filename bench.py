@@ -47,6 +47,10 @@ CONFIGS = {
                desc="Mistral-7B GQA decode attention, B=64, S=16K, 4 of 32 layers"),
     "TGT": dict(layers=4, B=16, Hq=32, Hkv=32, D=128, S=32768, k_f=0.25, d_f=0.25, base=10000.0,
                 desc="north-star target: MHA 32 heads, B=16, S=32K, 4 layers"),
+    # C5 is sharded by KV head over 8 GPUs: one GPU's shard = 1 KV head with its 8 query heads
+    "C5s": dict(layers=2, B=128, Hq=8, Hkv=1, D=128, S=131072, k_f=0.25, d_f=0.25, base=500000.0,
+                desc="Llama3-70B-shaped decode attention, one GPU's shard of 8 (1 KV head, 8 q heads), "
+                     "B=128, S=128K, 2 layers"),
 }
 
 

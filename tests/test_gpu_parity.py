@@ -461,3 +461,23 @@ def test_decoder_step_with_rope_gqa(mode):
 def _topk_of(q_hat, Kt, Vt, S, k):
     _, diag = L.loki_decode(q_hat, Kt, Vt, None, d=32, k=k, diagnostics=True)
     return diag.indices.cpu().numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"LOKI_SPLITK": "1"}, {"LOKI_PIPE_BIG": "1"}, {"LOKI_SPEC": "1"},
+                                 {"LOKI_PIPE_LA": "8192"}, {"LOKI_PIPE": "0"}])
+def test_pipe_variants_match_oracle(env, monkeypatch):
+    """The pipe kernel's opt-in variants (split-K tensor-core phase 3, 8192-row chunks, speculative
+    boundary candidates, large A chunks) and the cluster kernel give the same parity on MHA and GQA."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for B, Hq, Hkv, S in [(2, 2, 2, 8192), (2, 4, 1, 5000)]:
+        q, K, V = make_batch(B, Hq, Hkv, 128, S, seed=S + Hq, bf16=True)
+        cfg = L.LokiConfig(k_f=0.25, d_f=0.25)
+        y, diag = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+                                torch.from_numpy(V).to(DEV, torch.bfloat16), None, cfg=cfg, diagnostics=True)
+        d, k = cfg.resolve(128, S)
+        check_sets_and_outputs(q, K, V, [S] * B, d, [k] * B, diag.indices.cpu().numpy(), y.cpu().numpy(), 1e-3)
+        y2 = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
+                           torch.from_numpy(V).to(DEV, torch.bfloat16), None, cfg=cfg)  # no diagnostics
+        assert O.rel_err(y2.cpu().numpy(), y.cpu().numpy()) <= 1e-5
