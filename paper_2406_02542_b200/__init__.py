@@ -61,7 +61,15 @@ from .kernels import (
     sliced_score_kernel,
 )
 from .linalg import canonicalize_indices, softmax_row, softmax_rows, topk_indices, topk_rows
-from .metrics import exact_speedup, jaccard_topk, theoretical_speedup
+from .metrics import (
+    AgreementCell,
+    AgreementStats,
+    agreement_sweep,
+    exact_speedup,
+    jaccard_topk,
+    score_error,
+    theoretical_speedup,
+)
 from .rope import RopeParams, rope_angles, rope_apply, rope_apply_rows
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -481,3 +481,25 @@ def test_pipe_variants_match_oracle(env, monkeypatch):
         y2 = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, torch.bfloat16),
                            torch.from_numpy(V).to(DEV, torch.bfloat16), None, cfg=cfg)  # no diagnostics
         assert O.rel_err(y2.cpu().numpy(), y.cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_agreement_sweep_matches_reference_algorithm():
+    """metrics.agreement_sweep (metrics.py:93-133) on the device vs the same computation in numpy."""
+    rng = np.random.default_rng(5)
+    S, D, m = 2048, 128, 12
+    keys = O.gen_synthetic_keys(S + 512, D, 16, 1e-3, 9)
+    P, _ = O.build_projection(keys[:512])
+    K = keys[512:].astype(np.float32)
+    V = rng.standard_normal((S, D)).astype(np.float32)
+    Q = rng.standard_normal((m, D)).astype(np.float32)
+    stats = L.agreement_sweep(K, V, Q, P, [0.125, 0.25], [0.25, 0.5])
+    Kh, Qh = (K @ P).astype(np.float32), (Q @ P).astype(np.float32)
+    exact = Q @ K.T
+    for c in stats.cells:
+        d, k = L.LokiConfig(k_f=c.k_f, d_f=c.d_f).resolve(D, S)
+        approx = Qh[:, :d] @ Kh[:, :d].T
+        jac = [L.jaccard_topk(O.topk_indices(approx[i], k), O.topk_indices(exact[i], k)) for i in range(m)]
+        assert abs(c.mean_jaccard - np.mean(jac)) <= 2.0 / k, (c, np.mean(jac))
+        assert abs(c.min_jaccard - np.min(jac)) <= 4.0 / k, (c, np.min(jac))
+    assert "mean_jaccard" in stats.to_tsv()
