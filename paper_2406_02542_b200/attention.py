@@ -443,15 +443,18 @@ class LokiDecoder:
         self.out = out if out is not None else torch.empty((B, Hq, D), dtype=torch.float32, device=self.device)
         self.P_stride = P.stride(0) if (P is not None and P.dim() == 3) else 0
         self.dense = dense
+        self._append_args = None
         self.call = _core.DecodeCall(self.q_hat, K, V, lens, S_max, d, k_f=k_f or 0.0, k_fixed=k or 0,
                                      select_mode=_lib.SELECT_ALL if dense else _lib.SELECT_TOPK, out=self.out,
                                      Hq=Hq, cluster=cluster)
 
     def append(self, stream):
-        _lib.check(self.lib.loki_append_kv(
-            _lib.ptr(self.q_raw), _lib.ptr(self.k_raw), _lib.ptr(self.v_new), _lib.ptr(self.P), self.P_stride,
-            _lib.ptr(self.inv), _lib.ptr(self.positions), self.rope_mode, self.K.data_ptr(), self.V.data_ptr(),
-            self.geom, self.rows.data_ptr(), self.q_hat.data_ptr(), stream))
+        if self._append_args is None:  # pointers are stable: build the argument list once
+            self._append_args = (
+                _lib.ptr(self.q_raw), _lib.ptr(self.k_raw), _lib.ptr(self.v_new), _lib.ptr(self.P), self.P_stride,
+                _lib.ptr(self.inv), _lib.ptr(self.positions), self.rope_mode, self.K.data_ptr(), self.V.data_ptr(),
+                self.geom, self.rows.data_ptr(), self.q_hat.data_ptr())
+        _lib.check(self.lib.loki_append_kv(*self._append_args, stream))
 
     def attend(self, stream):
         self.call.run(stream)
