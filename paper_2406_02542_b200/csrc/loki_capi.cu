@@ -323,8 +323,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
   // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn
-  // (r01 sweeps: MHA best at 4.0; G = 4 best at 7-10, tools/lag_sweep.sh)
-  const double lagx = env_int("LOKI_PIPE_LAG_X10", G == 1 ? 40 : 25 * G) / 10.0;
+  // (r01 sweeps, tools/lag_sweep.sh: MHA best at 4.0; G = 4 at 7-10; G = 8 (C5s) at 32)
+  const double lagx = env_int("LOKI_PIPE_LAG_X10", G == 1 ? 40 : (G <= 4 ? 25 * G : 40 * G)) / 10.0;
   const int per_slot = (p.nAa + p.nA) > 2 * p.nA ? (p.nAa + p.nA) : 2 * p.nA;
   int lag = (int)ceil(lagx * pl->grid / (double)(p.nAa + p.nA));
   p.lag = lag < 1 ? 1 : (lag > units ? units : lag);
