@@ -503,3 +503,36 @@ def test_agreement_sweep_matches_reference_algorithm():
         assert abs(c.mean_jaccard - np.mean(jac)) <= 2.0 / k, (c, np.mean(jac))
         assert abs(c.min_jaccard - np.min(jac)) <= 4.0 / k, (c, np.min(jac))
     assert "mean_jaccard" in stats.to_tsv()
+
+
+PIPE_GEOMETRY = [  # D, Hq, Hkv, dtype, d: every consumer variant of the pipe kernel
+    (128, 2, 2, "bf16", 32),   # lane-per-row phase 1 (64 B rows), tensor-core phase 3
+    (128, 2, 2, "bf16", 64),   # lane-per-row phase 1 (128 B rows)
+    (128, 2, 2, "bf16", 16),   # SIMT phase 1 (32 B rows)
+    (128, 4, 2, "bf16", 32),   # G = 2 tensor-core phase 1
+    (128, 8, 2, "bf16", 64),   # G = 4
+    (128, 8, 1, "bf16", 32),   # G = 8 (heads in n-tiles, hi / lo in two mmas)
+    (64, 4, 4, "bf16", 16),    # D = 64
+    (64, 8, 2, "bf16", 32),
+    (256, 2, 2, "bf16", 64),   # D = 256
+    (256, 8, 2, "bf16", 64),
+    (128, 2, 2, "f32", 32),    # fp32 caches: SIMT phase 3
+    (128, 8, 2, "f32", 32),
+    (64, 8, 1, "f32", 16),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("geom", PIPE_GEOMETRY, ids=lambda g: "D%d_Hq%d_Hkv%d_%s_d%d" % g)
+def test_pipe_geometry_matrix(geom):
+    D, Hq, Hkv, dt, d = geom
+    bf = dt == "bf16"
+    S_cap = 9000
+    lens = [9000, 4097, 1, 2048]  # ragged: several chunks, a partial chunk, one row, one chunk
+    q, K, V = make_batch(4, Hq, Hkv, D, S_cap, seed=D + 10 * Hq + d, bf16=bf)
+    tdt = torch.bfloat16 if bf else torch.float32
+    k_f = 0.25
+    y, diag = L.loki_decode(torch.from_numpy(q).to(DEV), torch.from_numpy(K).to(DEV, tdt),
+                            torch.from_numpy(V).to(DEV, tdt), lens, d=d, k_f=k_f, diagnostics=True)
+    ks = [L.resolve_fraction(k_f, s) for s in lens]
+    check_sets_and_outputs(q, K, V, lens, d, ks, diag.indices.cpu().numpy(), y.cpu().numpy(), 1e-3)
