@@ -1,3 +1,8 @@
-# lag (LOKI_PIPE_LAG_X10) sweep for the C5s shard (GQA 8, S = 128K, 128 units)
-for l in 200 320 640 2000; do echo c5s-lag$l; LOKI_PIPE_LAG_X10=$l python tools/one_layer.py --B 128 --H 8 --Hkv 1 --S 131072 --reps 3 | tail -1; done
-echo c5s-trace; LOKI_TRACE=1 python tools/one_layer.py --B 128 --H 8 --Hkv 1 --S 131072 --reps 2 | grep -v "CTAs in"
+# TGT chunking sweep (host knobs only): A chunk rows x B part rows x split-K
+for i in 1 2; do
+echo big; python tools/one_layer.py --S 32768 --reps 10 | tail -1
+echo la8192; LOKI_PIPE_BIG=0 LOKI_PIPE_LA=8192 python tools/one_layer.py --S 32768 --reps 10 | tail -1
+echo la8192-split; LOKI_PIPE_BIG=0 LOKI_PIPE_LA=8192 LOKI_SPLITK=1 python tools/one_layer.py --S 32768 --reps 10 | tail -1
+echo la16384; LOKI_PIPE_BIG=0 LOKI_PIPE_LA=16384 python tools/one_layer.py --S 32768 --reps 10 | tail -1
+echo big-la16384; LOKI_PIPE_LA=16384 python tools/one_layer.py --S 32768 --reps 10 | tail -1
+done
