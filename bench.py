@@ -626,7 +626,7 @@ def main():
                          "dense_achieved_gbs": round(dense_bytes / (dense_attn_us * 1e-6) / 1e9, 1)},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 * wl.L * args.steps,
+            "gpu_launches": (1 + (2 if plan["ctas_per_unit"] == -2 else 1)) * wl.L * args.steps,
             "clocks": clocks_rec,
             "timing": f"{mode}; CUDA events on the launching stream, barrier + sync both sides, max over ranks",
             "plan": plan,

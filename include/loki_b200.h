@@ -112,7 +112,9 @@ loki_status loki_decode(const loki_decode_args* args, void* stream);
  * workspace between launches that may run concurrently. */
 loki_status loki_decode_workspace_bytes(const loki_decode_args* args, size_t* bytes);
 
-/* Launch plan chosen for `args`: CTAs per unit, rows per CTA, dynamic smem. */
+/* Launch plan chosen for `args`: CTAs per unit (cluster kernels), 0 for the
+ * persistent pipe kernel (one launch) or -2 for split pipe layers (an A-only and
+ * a B-only launch); rows per CTA / chunk; dynamic smem. */
 loki_status loki_decode_plan(const loki_decode_args* args, int32_t* ctas_per_unit,
                              int32_t* rows_per_cta, size_t* smem_bytes);
 

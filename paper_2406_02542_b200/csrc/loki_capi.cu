@@ -238,7 +238,9 @@ struct PipePlan {
   TmaGeom tg{};
   int G_T = 1;
   bool big = false;
-  int grid = 0;
+  bool split = false;  // A-only launch + B-only launch (MHA bf16)
+  int grid = 0, grid1 = 0, grid2 = 0;
+  size_t smem1 = 0;
   size_t smem = 0;
   size_t ws = 0;
   size_t off_hist = 0, off_keys = 0, off_tcs = 0, off_poff = 0, off_part = 0, off_spec = 0, off_logits = 0;
@@ -320,6 +322,16 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if (pl->smem > kSmemMax) return fail(LOKI_ERR_UNSUPPORTED, "pipe: shared memory plan %zu bytes", pl->smem);
   const int occ = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem, pl->big);
   if (occ < 1) return fail(LOKI_ERR_UNSUPPORTED, "pipe: kernel does not fit on an SM (%zu B smem)", pl->smem);
+  // r01: split layers beat the single launch on MHA bf16 (C2 212 -> 205 us, TGT 626 -> 603 us)
+  pl->split = env_int("LOKI_PIPE_SPLIT", 1) != 0 && G_T == 1 && g.dtype == LOKI_DTYPE_BF16 && !p.spec;
+  if (pl->split) {  // the A-only launch needs no B-item entry region
+    pl->smem1 = (size_t)p.off_ents + 1024;
+    const int occ1 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem1, pl->big, 1);
+    const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem, pl->big, 2);
+    if (occ1 < 1 || occ2 < 1) pl->split = false;
+    pl->grid1 = sm_count() * occ1;
+    pl->grid2 = sm_count() * occ2;
+  }
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
   // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn
@@ -331,7 +343,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   p.n_tickets = (long long)(units + p.lag) * per_slot;
   // workspace: ctrl | hist | keys | sel | part | logits
   const int HB = 1 << p.hbits;
-  size_t off = loki::align_up((size_t)(2 + 4 * (size_t)units) * 4, 256);
+  size_t off = loki::align_up((size_t)(2 + 4 * (size_t)units + 2) * 4, 256);  // + split-layer B counters
   pl->off_hist = off;
   off = loki::align_up(off + (size_t)units * G * HB * 4, 256);
   pl->off_keys = off;
@@ -400,7 +412,20 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   loki::TmaDesc maps[4];
   if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, p.mma != 0, p.lead_swz, maps))
     return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
-  cudaError_t e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big);
+  cudaError_t e;
+  if (pl.split) {
+    loki::PipeParams pa = p, pb = p;
+    pa.trace = pb.trace = nullptr;
+    pa.n_tickets = (long long)p.units * p.nAa;
+    int tail = loki::ceil_div(pl.grid2, p.nA);  // units whose B parts run as halves (short drain)
+    pb.lag = tail > p.units ? p.units : tail;
+    pb.n_tickets = (long long)(p.units - pb.lag) * p.nA + (long long)pb.lag * 2 * p.nA;
+    e = loki::launch_pipe(pa, g.dtype, pl.G_T, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big, 1);
+    if (e == cudaSuccess)
+      e = loki::launch_pipe(pb, g.dtype, pl.G_T, pl.grid2, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big, 2);
+  } else {
+    e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big);
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   return cuda_status(e, "loki_decode (pipe) launch");
 }
@@ -447,8 +472,8 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
   PipePlan pl;
-  if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {  // persistent grid: 0 CTAs per unit
-    if (ctas_per_unit) *ctas_per_unit = 0;
+  if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {  // persistent grid: 0 (-2: split, two launches)
+    if (ctas_per_unit) *ctas_per_unit = pl.split ? -2 : 0;
     if (rows_per_cta) *rows_per_cta = pl.p.Lc;
     if (smem_bytes) *smem_bytes = pl.smem;
     return LOKI_OK;

@@ -154,9 +154,10 @@ bool pipe_supported(int dtype, int D, int G_T);
 bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, int r1, int kcol0, bool mma,
                      int lead_swz, TmaDesc* maps);
 // big: 2x larger chunks (compiled for G == 1 only; long sequences amortise per-item latency)
+// mode 0: one launch; 1 / 2: the A-only / B-only halves of a split layer (MHA bf16)
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
-                        cudaStream_t st, bool big);
-int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big);
+                        cudaStream_t st, bool big, int mode = 0);
+int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode = 0);
 int pipe_warps();
 // 128-row blocks per warp in a B part (Lc = blocks * 128 * warps), shared by kernel and host
 __host__ __device__ constexpr int pipe_blocks_per_warp(int G_T, bool big) {

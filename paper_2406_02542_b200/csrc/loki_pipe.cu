@@ -5,16 +5,16 @@
 
 namespace loki {
 
-cudaError_t pipe_launch_bf16_64(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
-int pipe_occ_bf16_64(int, size_t, bool);
-cudaError_t pipe_launch_bf16_128(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
-int pipe_occ_bf16_128(int, size_t, bool);
-cudaError_t pipe_launch_bf16_256(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
-int pipe_occ_bf16_256(int, size_t, bool);
-cudaError_t pipe_launch_f32_64(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
-int pipe_occ_f32_64(int, size_t, bool);
-cudaError_t pipe_launch_f32_128(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool);
-int pipe_occ_f32_128(int, size_t, bool);
+cudaError_t pipe_launch_bf16_64(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool, int);
+int pipe_occ_bf16_64(int, size_t, bool, int);
+cudaError_t pipe_launch_bf16_128(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool, int);
+int pipe_occ_bf16_128(int, size_t, bool, int);
+cudaError_t pipe_launch_bf16_256(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool, int);
+int pipe_occ_bf16_256(int, size_t, bool, int);
+cudaError_t pipe_launch_f32_64(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool, int);
+int pipe_occ_f32_64(int, size_t, bool, int);
+cudaError_t pipe_launch_f32_128(const PipeParams&, int, int, size_t, const TmaDesc*, cudaStream_t, bool, int);
+int pipe_occ_f32_128(int, size_t, bool, int);
 
 
 int pipe_warps() { return kPW; }
@@ -44,27 +44,27 @@ bool pipe_supported(int dtype, int D, int G_T) {
   return (D == 64 || D == 128) && G_T <= 8;
 }
 
-int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big) {
+int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode) {
   if (dtype == LOKI_DTYPE_BF16) {
-    if (D == 64) return pipe_occ_bf16_64(G_T, smem, big);
-    if (D == 128) return pipe_occ_bf16_128(G_T, smem, big);
-    if (D == 256) return pipe_occ_bf16_256(G_T, smem, big);
+    if (D == 64) return pipe_occ_bf16_64(G_T, smem, big, mode);
+    if (D == 128) return pipe_occ_bf16_128(G_T, smem, big, mode);
+    if (D == 256) return pipe_occ_bf16_256(G_T, smem, big, mode);
   } else {
-    if (D == 64) return pipe_occ_f32_64(G_T, smem, big);
-    if (D == 128) return pipe_occ_f32_128(G_T, smem, big);
+    if (D == 64) return pipe_occ_f32_64(G_T, smem, big, mode);
+    if (D == 128) return pipe_occ_f32_128(G_T, smem, big, mode);
   }
   return 0;
 }
 
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
-                        cudaStream_t st, bool big) {
+                        cudaStream_t st, bool big, int mode) {
   if (dtype == LOKI_DTYPE_BF16) {
-    if (p.D == 64) return pipe_launch_bf16_64(p, G_T, grid, smem, maps, st, big);
-    if (p.D == 128) return pipe_launch_bf16_128(p, G_T, grid, smem, maps, st, big);
-    if (p.D == 256) return pipe_launch_bf16_256(p, G_T, grid, smem, maps, st, big);
+    if (p.D == 64) return pipe_launch_bf16_64(p, G_T, grid, smem, maps, st, big, mode);
+    if (p.D == 128) return pipe_launch_bf16_128(p, G_T, grid, smem, maps, st, big, mode);
+    if (p.D == 256) return pipe_launch_bf16_256(p, G_T, grid, smem, maps, st, big, mode);
   } else {
-    if (p.D == 64) return pipe_launch_f32_64(p, G_T, grid, smem, maps, st, big);
-    if (p.D == 128) return pipe_launch_f32_128(p, G_T, grid, smem, maps, st, big);
+    if (p.D == 64) return pipe_launch_f32_64(p, G_T, grid, smem, maps, st, big, mode);
+    if (p.D == 128) return pipe_launch_f32_128(p, G_T, grid, smem, maps, st, big, mode);
   }
   return cudaErrorInvalidValue;
 }

@@ -1485,8 +1485,12 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
 }
 
 // ------------------------------------------------------------------ kernel
-template <typename T, int G_T, int VEC, int D_T, bool BIG>
-__global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
+// MODE 0: one launch interleaves A and B tickets (lag).  Split layers (MODE 1 then MODE 2,
+// MHA bf16): an A-only launch (phase 1 + selection, 3 CTAs / SM) and a B-only launch (phase 3 +
+// merge) that starts as A CTAs retire, gated by the per-unit ready flags; it waits for the A
+// grid before it exits, so "B complete" implies "A complete" for whatever follows.
+template <typename T, int G_T, int VEC, int D_T, bool BIG, int MODE = 0>
+__global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(const PipeParams p,
                                                           const __grid_constant__ CUtensorMap lead_map,
                                                           const __grid_constant__ CUtensorMap krow_map,
                                                           const __grid_constant__ CUtensorMap vrow_map,
@@ -1518,11 +1522,50 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
     prefetch_desc(&vrow_map);
     prefetch_desc(&krow64_map);
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended rows are visible
+  // MODE 2 reads only what the ready flags publish (and K0's products, complete before the A grid
+  // passed its own wait): it does not wait for the A grid here
+  if constexpr (MODE != 2) asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended rows
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (tid == 0) sh.next_ticket = atomicAdd(&p.ctrl[0], 1u);
+  uint32_t* tk = MODE == 2 ? p.ctrl + 2 + 4 * (size_t)p.units : p.ctrl;  // ticket / exit counters
+  if (tid == 0) sh.next_ticket = atomicAdd(&tk[0], 1u);
   __syncthreads();
   RingPos rp(nsw);
+  if constexpr (MODE != 0) {
+    // MODE 1: tickets = A(u, c); MODE 2: full B parts of units [0, units - tail), then half parts
+    const int tailU = p.lag;  // (MODE 2: units whose parts run as halves)
+    const long long nfull = (long long)(p.units - tailU) * p.nA;
+    for (;;) {
+      const unsigned t = sh.next_ticket;
+      __syncthreads();
+      if ((long long)t >= p.n_tickets) {
+        if (tid == 0 && atomicAdd(&tk[1], 1u) == gridDim.x - 1u) {  // last CTA out resets the counters
+          atomicExch(&tk[0], 0u);
+          atomicExch(&tk[1], 0u);
+        }
+        break;
+      }
+      if (tid == 0) sh.next_ticket = atomicAdd(&tk[0], 1u);
+      if constexpr (MODE == 1) {
+        item_A<T, G_T, VEC>(p, &lead_map, (int)(t / (unsigned)p.nAa), (int)(t % (unsigned)p.nAa), ring, wring, wbar,
+                            hist, ents, sbar, sphase, rp, sh);
+      } else {
+        if ((long long)t < nfull) {
+          item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, (int)(t / (unsigned)p.nA),
+                                        (int)(t % (unsigned)p.nA), -1, ring, wring, wbar, ents, rp, sh);
+        } else {
+          const long long tt = t - nfull;
+          const int r = (int)(tt % (2 * p.nA));
+          item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map,
+                                        p.units - tailU + (int)(tt / (2 * p.nA)), r >> 1, r & 1, ring, wring, wbar,
+                                        ents, rp, sh);
+        }
+      }
+      fence_proxy_async();
+      __syncthreads();
+    }
+    if constexpr (MODE == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   // slot = A(u, 0..nAa-1), B(u - lag, 0..nA-1); tail slots (no A left): 2 nA half-size B items
   const int per_slot = max(p.nAa + p.nA, 2 * p.nA);
   for (;;) {
@@ -1566,9 +1609,9 @@ __global__ void __launch_bounds__(kPT, 2) pipe_decode_kernel(const PipeParams p,
 }  // namespace
 
 
-template <typename T, int G_T, int VEC, int D_T, bool BIG>
+template <typename T, int G_T, int VEC, int D_T, bool BIG, int MODE = 0>
 inline cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st) {
-  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG>;
+  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG, MODE>;
   static size_t smem_set = 0;
   if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1589,9 +1632,9 @@ inline cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, con
   return cudaLaunchKernelEx(&cfg, kern, p, m[0], m[1], m[2], m[3]);
 }
 
-template <typename T, int G_T, int VEC, int D_T, bool BIG>
+template <typename T, int G_T, int VEC, int D_T, bool BIG, int MODE = 0>
 inline int occupancy_t(size_t smem) {
-  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG>;
+  auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG, MODE>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kPT, smem) != cudaSuccess) return 0;
@@ -1603,8 +1646,19 @@ inline int occupancy_t(size_t smem) {
 // its own translation unit (loki_pipe_inst_*.cu) so the build runs in parallel.
 template <typename T, int DT>
 cudaError_t pipe_launch_dt(const PipeParams& p, int G_T, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st,
-                           bool big) {
+                           bool big, int mode) {
   constexpr int V = sizeof(T) == 2 ? 8 : 4;
+  if constexpr (sizeof(T) == 2) {  // split layers: MHA bf16 only
+    if (mode != 0) {
+      if (G_T != 1) return cudaErrorInvalidValue;
+      if (mode == 1)
+        return big ? launch_pipe_t<T, 1, V, DT, true, 1>(p, grid, smem, maps, st)
+                   : launch_pipe_t<T, 1, V, DT, false, 1>(p, grid, smem, maps, st);
+      return big ? launch_pipe_t<T, 1, V, DT, true, 2>(p, grid, smem, maps, st)
+                 : launch_pipe_t<T, 1, V, DT, false, 2>(p, grid, smem, maps, st);
+    }
+  }
+  if (mode != 0) return cudaErrorInvalidValue;
   switch (G_T) {
     case 1:
       return big ? launch_pipe_t<T, 1, V, DT, true>(p, grid, smem, maps, st)
@@ -1619,8 +1673,16 @@ cudaError_t pipe_launch_dt(const PipeParams& p, int G_T, int grid, size_t smem, 
   return cudaErrorInvalidValue;
 }
 template <typename T, int DT>
-int pipe_occ_dt(int G_T, size_t smem, bool big) {
+int pipe_occ_dt(int G_T, size_t smem, bool big, int mode) {
   constexpr int V = sizeof(T) == 2 ? 8 : 4;
+  if constexpr (sizeof(T) == 2) {
+    if (mode != 0) {
+      if (G_T != 1) return 0;
+      if (mode == 1) return big ? occupancy_t<T, 1, V, DT, true, 1>(smem) : occupancy_t<T, 1, V, DT, false, 1>(smem);
+      return big ? occupancy_t<T, 1, V, DT, true, 2>(smem) : occupancy_t<T, 1, V, DT, false, 2>(smem);
+    }
+  }
+  if (mode != 0) return 0;
   switch (G_T) {
     case 1: return big ? occupancy_t<T, 1, V, DT, true>(smem) : occupancy_t<T, 1, V, DT, false>(smem);
     case 2: return occupancy_t<T, 2, V, DT, false>(smem);
@@ -1635,9 +1697,11 @@ int pipe_occ_dt(int G_T, size_t smem, bool big) {
 
 #define LOKI_PIPE_SLICE(NAME, T, DT)                                                                        \
   cudaError_t pipe_launch_##NAME(const PipeParams& p, int G_T, int grid, size_t smem, const TmaDesc* maps,  \
-                                 cudaStream_t st, bool big) {                                               \
-    return pipe_launch_dt<T, DT>(p, G_T, grid, smem, maps, st, big);                                        \
+                                 cudaStream_t st, bool big, int mode) {                                     \
+    return pipe_launch_dt<T, DT>(p, G_T, grid, smem, maps, st, big, mode);                                  \
   }                                                                                                         \
-  int pipe_occ_##NAME(int G_T, size_t smem, bool big) { return pipe_occ_dt<T, DT>(G_T, smem, big); }
+  int pipe_occ_##NAME(int G_T, size_t smem, bool big, int mode) {                                           \
+    return pipe_occ_dt<T, DT>(G_T, smem, big, mode);                                                        \
+  }
 
 }  // namespace loki

@@ -59,7 +59,7 @@ torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1000 / a.reps
 print(f"{a.mode}: {us:.1f} us/launch, {nbytes / us / 1e3:.1f} GB/s algorithmic")
 
-if os.environ.get("LOKI_TRACE") and call.plan()["ctas_per_unit"] == 0:
+if os.environ.get("LOKI_TRACE") and call.plan()["ctas_per_unit"] <= 0:
     # persistent pipe kernel: per-ticket {start, end, smid | kind << 16 | block << 32}
     import numpy as np
 
