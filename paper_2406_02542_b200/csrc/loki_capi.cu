@@ -323,13 +323,21 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   const int occ = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem, pl->big);
   if (occ < 1) return fail(LOKI_ERR_UNSUPPORTED, "pipe: kernel does not fit on an SM (%zu B smem)", pl->smem);
   // r01: split layers beat the single launch on MHA bf16 (C2 212 -> 205 us, TGT 626 -> 603 us)
-  pl->split = env_int("LOKI_PIPE_SPLIT", 1) != 0 && G_T == 1 && g.dtype == LOKI_DTYPE_BF16 && !p.spec;
+  // (short sequences keep one launch: S = 4K 125 vs 137 us split)
+  pl->split = env_int("LOKI_PIPE_SPLIT", a->S_max >= 8192 ? 1 : 0) != 0 && G_T == 1 &&
+              g.dtype == LOKI_DTYPE_BF16 && !p.spec;
   if (pl->split) {  // the A-only launch needs no B-item entry region
     pl->smem1 = (size_t)p.off_ents + 1024;
     const int occ1 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem1, pl->big, 1);
     const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem, pl->big, 2);
     if (occ1 < 1 || occ2 < 1) pl->split = false;
-    pl->grid1 = sm_count() * occ1;
+    // A chunks of >= 8192 rows (r01: C2 197.9 -> 193.0 us); the A launch has no lag to feed
+    if (env_int("LOKI_PIPE_LA", 0) == 0 && p.La < 8192) {
+      p.La = 8192;
+      p.nAa = loki::ceil_div(a->S_max, p.La);
+    }
+    const int a_ctas = env_int("LOKI_PIPE_A_CTAS", occ1);
+    pl->grid1 = sm_count() * (a_ctas < occ1 ? (a_ctas < 1 ? 1 : a_ctas) : occ1);
     pl->grid2 = sm_count() * occ2;
   }
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
@@ -417,7 +425,9 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
     loki::PipeParams pa = p, pb = p;
     pa.trace = pb.trace = nullptr;
     pa.n_tickets = (long long)p.units * p.nAa;
-    int tail = loki::ceil_div(pl.grid2, p.nA);  // units whose B parts run as halves (short drain)
+    // units whose B parts run as halves (short drain): about one wave of CTAs
+    // (r01 sweep: 0.2 waves best; 1 wave costs C2 7 us)
+    int tail = (int)ceil(env_int("LOKI_PIPE_TAIL_X10", 2) / 10.0 * pl.grid2 / p.nA);
     pb.lag = tail > p.units ? p.units : tail;
     pb.n_tickets = (long long)(p.units - pb.lag) * p.nA + (long long)pb.lag * 2 * p.nA;
     e = loki::launch_pipe(pa, g.dtype, pl.G_T, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big, 1);

@@ -1,8 +1,7 @@
-# TGT chunking sweep (host knobs only): A chunk rows x B part rows x split-K
-for i in 1 2; do
-echo big; python tools/one_layer.py --S 32768 --reps 10 | tail -1
-echo la8192; LOKI_PIPE_BIG=0 LOKI_PIPE_LA=8192 python tools/one_layer.py --S 32768 --reps 10 | tail -1
-echo la8192-split; LOKI_PIPE_BIG=0 LOKI_PIPE_LA=8192 LOKI_SPLITK=1 python tools/one_layer.py --S 32768 --reps 10 | tail -1
-echo la16384; LOKI_PIPE_BIG=0 LOKI_PIPE_LA=16384 python tools/one_layer.py --S 32768 --reps 10 | tail -1
-echo big-la16384; LOKI_PIPE_LA=16384 python tools/one_layer.py --S 32768 --reps 10 | tail -1
-done
+# split-layer defaults confirmation (C2, TGT, S = 16K, S = 4K) and parity
+python -m pytest tests -m gpu -x -q --tb=short 2>&1 | tail -2
+for i in 1 2; do echo c2; python tools/one_layer.py --reps 20 | tail -1; done
+echo tgt; python tools/one_layer.py --S 32768 --reps 10 | tail -1
+echo s16k; python tools/one_layer.py --S 16384 --reps 10 | tail -1
+echo s4k; python tools/one_layer.py --S 4096 --reps 20 | tail -1
+echo s4k-comb; LOKI_PIPE_SPLIT=0 python tools/one_layer.py --S 4096 --reps 20 | tail -1
