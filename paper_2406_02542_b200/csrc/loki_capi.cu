@@ -324,8 +324,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if (occ < 1) return fail(LOKI_ERR_UNSUPPORTED, "pipe: kernel does not fit on an SM (%zu B smem)", pl->smem);
   // r01: split layers beat the single launch on MHA bf16 (C2 212 -> 205 us, TGT 626 -> 603 us)
   // (short sequences keep one launch: S = 4K 125 vs 137 us split)
-  pl->split = env_int("LOKI_PIPE_SPLIT", a->S_max >= 8192 ? 1 : 0) != 0 && G_T == 1 &&
-              g.dtype == LOKI_DTYPE_BF16 && !p.spec;
+  // (r01: GQA too, C3 866 -> 742, C4 989 -> 875, C5s 4445 -> 3468 us)
+  pl->split = env_int("LOKI_PIPE_SPLIT", a->S_max >= 8192 ? 1 : 0) != 0 && g.dtype == LOKI_DTYPE_BF16 && !p.spec;
   if (pl->split) {  // the A-only launch needs no B-item entry region
     pl->smem1 = (size_t)p.off_ents + 1024;
     const int occ1 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem1, pl->big, 1);
@@ -340,13 +340,20 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
     pl->grid1 = sm_count() * (a_ctas < occ1 ? (a_ctas < 1 ? 1 : a_ctas) : occ1);
     pl->grid2 = sm_count() * occ2;
   }
+  // B parts as halves (1: the tail units, which shortens the drain; 2: every unit; 0: none).  r01 sweep
+  // (tools/halves_check.sh): one launch gains from tail halves (S = 4K 137 -> 125 us, B = 1 48 -> 40,
+  // GQA 186 -> 163); split layers lose from either (TGT 597 / 593 / 641 us).  With tail halves the
+  // grouping of a unit's partial states depends on the number of units, so KV-head shards agree with one
+  // launch to rounding, not bit for bit (0 or 2 keep them bit-identical)
+  p.halves = env_int("LOKI_PIPE_HALVES", pl->split ? 0 : 1);
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
   // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn
   // (r01 sweeps, tools/lag_sweep.sh: MHA best at 4.0; G = 4 at 7-10; G = 8 (C5s) at 32)
   const double lagx = env_int("LOKI_PIPE_LAG_X10", G == 1 ? 40 : (G <= 4 ? 25 * G : 40 * G)) / 10.0;
-  const int per_slot = (p.nAa + p.nA) > 2 * p.nA ? (p.nAa + p.nA) : 2 * p.nA;
-  int lag = (int)ceil(lagx * pl->grid / (double)(p.nAa + p.nA));
+  const int nb_slot = (p.halves == 2 ? 2 : 1) * p.nA;  // B tickets per unit
+  const int per_slot = (p.nAa + nb_slot) > 2 * p.nA ? (p.nAa + nb_slot) : 2 * p.nA;
+  int lag = (int)ceil(lagx * pl->grid / (double)(p.nAa + nb_slot));
   p.lag = lag < 1 ? 1 : (lag > units ? units : lag);
   p.n_tickets = (long long)(units + p.lag) * per_slot;
   // workspace: ctrl | hist | keys | sel | part | logits
@@ -425,9 +432,10 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
     loki::PipeParams pa = p, pb = p;
     pa.trace = pb.trace = nullptr;
     pa.n_tickets = (long long)p.units * p.nAa;
-    // units whose B parts run as halves (short drain): about one wave of CTAs
-    // (r01 sweep: 0.2 waves best; 1 wave costs C2 7 us)
-    int tail = (int)ceil(env_int("LOKI_PIPE_TAIL_X10", 2) / 10.0 * pl.grid2 / p.nA);
+    // units whose B parts run as halves (short drain, opt-in: the grouping of the partial states then
+    // depends on the number of units, so KV-head shards would not be bit-identical to one launch)
+    int tail = p.halves == 2 ? p.units
+               : p.halves ? (int)ceil(env_int("LOKI_PIPE_TAIL_X10", 2) / 10.0 * pl.grid2 / p.nA) : 0;
     pb.lag = tail > p.units ? p.units : tail;
     pb.n_tickets = (long long)(p.units - pb.lag) * p.nA + (long long)pb.lag * 2 * p.nA;
     e = loki::launch_pipe(pa, g.dtype, pl.G_T, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big, 1);

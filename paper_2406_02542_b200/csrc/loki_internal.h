@@ -90,6 +90,7 @@ struct PipeParams {
   uint32_t* cwin;    // [units][G][nA] each chunk's bin window lo | hi << 16
   long long* trace;  // optional [n_tickets][4] {start, end, sm | kind << 16 | block << 32, tail start}
   int debug;
+  int halves;        // B parts in halves: 2 every unit, 1 tail units only (grouping then depends on #units), 0 none
 };
 
 // Phase-trace buffer installed by loki_set_phase_trace (diagnostics only).

@@ -869,7 +869,8 @@ __device__ void merge_unit(const PipeParams& p, int u, int S, PipeShared& sh) {
   const int G = p.G, D = p.D, ldp = D + 2;
   uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
   const size_t qrow0 = ((size_t)(u / p.Hkv) * p.Hq) + (size_t)(u % p.Hkv) * G;
-  const bool split = u + p.lag >= p.units;  // tail units run half-size B items
+  // half-size B parts: every unit (halves == 2) or the tail units (halves == 1)
+  const bool split = p.halves == 2 || (p.halves == 1 && u + p.lag >= p.units);
   const int nparts = ceil_div(S > 0 ? S : 1, p.Lc) * (split ? 2 : 1);
   const float* part = p.part + (size_t)u * 2 * p.nA * G * ldp;
   for (int i = tid; i < G * D; i += kPT) {
@@ -1567,7 +1568,7 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
     return;
   }
   // slot = A(u, 0..nAa-1), B(u - lag, 0..nA-1); tail slots (no A left): 2 nA half-size B items
-  const int per_slot = max(p.nAa + p.nA, 2 * p.nA);
+  const int per_slot = max(p.nAa + (p.halves == 2 ? 2 : 1) * p.nA, 2 * p.nA);
   for (;;) {
     const unsigned t = sh.next_ticket;
     __syncthreads();
@@ -1582,15 +1583,18 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
     const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
     const int slot = (int)(t / (unsigned)per_slot), r = (int)(t % (unsigned)per_slot);
     int kind = 0;
-    if (slot >= p.units) {  // tail slot: no A items left, half-size B items
-      if (r < 2 * p.nA)
-        kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r >> 1, r & 1, ring, wring, wbar, ents,
+    if (slot >= p.units) {  // tail slot: no A items left, B items (half-size with p.halves)
+      if (p.halves ? r < 2 * p.nA : r < p.nA)
+        kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag,
+                                      p.halves ? r >> 1 : r, p.halves ? (r & 1) : -1, ring, wring, wbar, ents,
                                       rp, sh);
     } else if (r < p.nAa) {
       kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, sbar, sphase, rp, sh);
-    } else if (slot >= p.lag && r < p.nAa + p.nA) {
-      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag, r - p.nAa, -1, ring, wring, wbar, ents,
-                                      rp, sh);
+    } else if (slot >= p.lag && r < p.nAa + (p.halves == 2 ? 2 * p.nA : p.nA)) {
+      const int rb = r - p.nAa;
+      kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag,
+                                      p.halves == 2 ? rb >> 1 : rb, p.halves == 2 ? (rb & 1) : -1, ring, wring,
+                                      wbar, ents, rp, sh);
     }
     fence_proxy_async();  // this item's generic shared-memory writes precede the next item's TMA writes
     __syncthreads();
@@ -1648,14 +1652,29 @@ template <typename T, int DT>
 cudaError_t pipe_launch_dt(const PipeParams& p, int G_T, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st,
                            bool big, int mode) {
   constexpr int V = sizeof(T) == 2 ? 8 : 4;
-  if constexpr (sizeof(T) == 2) {  // split layers: MHA bf16 only
+  if constexpr (sizeof(T) == 2) {  // split layers: bf16 caches
     if (mode != 0) {
-      if (G_T != 1) return cudaErrorInvalidValue;
-      if (mode == 1)
-        return big ? launch_pipe_t<T, 1, V, DT, true, 1>(p, grid, smem, maps, st)
-                   : launch_pipe_t<T, 1, V, DT, false, 1>(p, grid, smem, maps, st);
-      return big ? launch_pipe_t<T, 1, V, DT, true, 2>(p, grid, smem, maps, st)
-                 : launch_pipe_t<T, 1, V, DT, false, 2>(p, grid, smem, maps, st);
+      switch (G_T) {
+        case 1:
+          if (mode == 1)
+            return big ? launch_pipe_t<T, 1, V, DT, true, 1>(p, grid, smem, maps, st)
+                       : launch_pipe_t<T, 1, V, DT, false, 1>(p, grid, smem, maps, st);
+          return big ? launch_pipe_t<T, 1, V, DT, true, 2>(p, grid, smem, maps, st)
+                     : launch_pipe_t<T, 1, V, DT, false, 2>(p, grid, smem, maps, st);
+        case 2:
+          return mode == 1 ? launch_pipe_t<T, 2, V, DT, false, 1>(p, grid, smem, maps, st)
+                           : launch_pipe_t<T, 2, V, DT, false, 2>(p, grid, smem, maps, st);
+        case 4:
+          return mode == 1 ? launch_pipe_t<T, 4, V, DT, false, 1>(p, grid, smem, maps, st)
+                           : launch_pipe_t<T, 4, V, DT, false, 2>(p, grid, smem, maps, st);
+        case 8:
+          if constexpr (DT != 256)
+            return mode == 1 ? launch_pipe_t<T, 8, 4, DT, false, 1>(p, grid, smem, maps, st)
+                             : launch_pipe_t<T, 8, 4, DT, false, 2>(p, grid, smem, maps, st);
+          break;
+        default: break;
+      }
+      return cudaErrorInvalidValue;
     }
   }
   if (mode != 0) return cudaErrorInvalidValue;
@@ -1677,9 +1696,19 @@ int pipe_occ_dt(int G_T, size_t smem, bool big, int mode) {
   constexpr int V = sizeof(T) == 2 ? 8 : 4;
   if constexpr (sizeof(T) == 2) {
     if (mode != 0) {
-      if (G_T != 1) return 0;
-      if (mode == 1) return big ? occupancy_t<T, 1, V, DT, true, 1>(smem) : occupancy_t<T, 1, V, DT, false, 1>(smem);
-      return big ? occupancy_t<T, 1, V, DT, true, 2>(smem) : occupancy_t<T, 1, V, DT, false, 2>(smem);
+      switch (G_T) {
+        case 1:
+          if (mode == 1) return big ? occupancy_t<T, 1, V, DT, true, 1>(smem) : occupancy_t<T, 1, V, DT, false, 1>(smem);
+          return big ? occupancy_t<T, 1, V, DT, true, 2>(smem) : occupancy_t<T, 1, V, DT, false, 2>(smem);
+        case 2: return mode == 1 ? occupancy_t<T, 2, V, DT, false, 1>(smem) : occupancy_t<T, 2, V, DT, false, 2>(smem);
+        case 4: return mode == 1 ? occupancy_t<T, 4, V, DT, false, 1>(smem) : occupancy_t<T, 4, V, DT, false, 2>(smem);
+        case 8:
+          if constexpr (DT != 256)
+            return mode == 1 ? occupancy_t<T, 8, 4, DT, false, 1>(smem) : occupancy_t<T, 8, 4, DT, false, 2>(smem);
+          break;
+        default: break;
+      }
+      return 0;
     }
   }
   if (mode != 0) return 0;
