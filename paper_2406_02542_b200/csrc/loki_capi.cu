@@ -340,12 +340,14 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
     pl->grid1 = sm_count() * (a_ctas < occ1 ? (a_ctas < 1 ? 1 : a_ctas) : occ1);
     pl->grid2 = sm_count() * occ2;
   }
-  // B parts as halves (1: the tail units, which shortens the drain; 2: every unit; 0: none).  r01 sweep
-  // (tools/halves_check.sh): one launch gains from tail halves (S = 4K 137 -> 125 us, B = 1 48 -> 40,
-  // GQA 186 -> 163); split layers lose from either (TGT 597 / 593 / 641 us).  With tail halves the
-  // grouping of a unit's partial states depends on the number of units, so KV-head shards agree with one
-  // launch to rounding, not bit for bit (0 or 2 keep them bit-identical)
-  p.halves = env_int("LOKI_PIPE_HALVES", pl->split ? 0 : 1);
+  // B parts as halves (2: every unit; 1: the tail units, which shortens the drain; 0: none).  r01 sweep
+  // (tools/halves_check.sh, one launch): every-unit halves help groups and small batches (GQA S = 4K
+  // 186 -> 166 us, B = 1 48 -> 40, B = 4 73 -> 70) but not B = 16 MHA (137 -> 136, S = 2K 95 -> 101);
+  // split layers lose from either (TGT 597 / 593 / 641 us).  The default depends on G, B and S only, so a
+  // KV-head shard groups its partial states exactly like one launch (bit-identical).  Tail
+  // halves (1) are faster still at one launch (S = 4K 137 -> 125 us, B = 4 73 -> 57) but the tail is a
+  // set of units, so shards then agree to rounding only: opt-in
+  p.halves = env_int("LOKI_PIPE_HALVES", pl->split ? 0 : ((G >= 2 || g.B <= 4) ? 2 : 0));
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
   // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn

@@ -77,18 +77,19 @@ def test_gloo_world2_shard_and_gather_equals_unsharded(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("halves", ["0", "2", None])
-def test_sharded_decode_bit_identical_on_gpu(monkeypatch, halves):
+@pytest.mark.parametrize("halves", ["0", "2", None, "1"])
+@pytest.mark.parametrize("B,Hq,Hkv", [(4, 16, 8), (8, 8, 8)])
+def test_sharded_decode_bit_identical_on_gpu(monkeypatch, halves, B, Hq, Hkv):
     """Units are independent: decoding each KV-head shard separately gives the
     same bits as one unsharded launch (what an N-GPU run computes per rank).
-    The default plan runs the tail units' parts as halves, whose grouping
-    depends on the number of units: shards then agree to rounding only."""
+    Opt-in tail halves (LOKI_PIPE_HALVES=1) split the parts of a set of tail
+    units, which depends on the number of units: shards then agree to rounding."""
     import paper_2406_02542_b200 as L
 
     if halves is not None:
         monkeypatch.setenv("LOKI_PIPE_HALVES", halves)
     dev = torch.device("cuda", 0)
-    B, Hq, Hkv, D, S = 4, 16, 8, 128, 4096
+    D, S = 128, 4096
     g = torch.Generator(device=dev).manual_seed(11)
     K = torch.randn(B, Hkv, S, D, device=dev, generator=g).to(torch.bfloat16)
     V = torch.randn(B, Hkv, S, D, device=dev, generator=g).to(torch.bfloat16)
@@ -104,7 +105,7 @@ def test_sharded_decode_bit_identical_on_gpu(monkeypatch, halves):
                                        None, cfg=cfg))
         torch.cuda.synchronize()
         y_sh = torch.cat(parts, dim=1)
-        if halves is None:
+        if halves == "1":
             assert torch.allclose(y_sh, y_full, rtol=1e-5, atol=1e-6), world
         else:
             assert torch.equal(y_sh, y_full), world
