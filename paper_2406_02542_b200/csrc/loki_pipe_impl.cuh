@@ -1196,8 +1196,12 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
                      : "=r"(a2[0]), "=r"(a2[1])
                      : "r"(addr));
         const uint32_t a[4] = {a2[0], 0u, a2[1], 0u};
-        mma_bf16(S, a, qb[ks][0], qb[ks][1]);
-        if (!kSplitCols) mma_bf16(S2, a, ql[ks][0], ql[ks][1]);
+        if (kSplitCols) {  // two accumulators (even / odd k-steps): half the dependent mma chain
+          mma_bf16((ks & 1) ? S2 : S, a, qb[ks][0], qb[ks][1]);
+        } else {
+          mma_bf16(S, a, qb[ks][0], qb[ks][1]);
+          mma_bf16(S2, a, ql[ks][0], ql[ks][1]);
+        }
       }
     }
     const int tA = st * R + g8;
@@ -1206,7 +1210,7 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
 #pragma unroll
     for (int j = 0; j < NHL; ++j) {
       const int head = kSplitCols ? t4 : 2 * t4 + j;
-      x[j] = kSplitCols ? S[0] + S[1] : S[j] + S2[j];
+      x[j] = kSplitCols ? (S[0] + S2[0]) + (S[1] + S2[1]) : S[j] + S2[j];
       const bool ok = head < G && ((eA >> (24 + head)) & 1u);
       if (split && ok) x[j] += apx[head * p.Lc + tA];  // phase-1 partial over the first d columns
       float tm = ok ? x[j] : -CUDART_INF_F;
