@@ -308,7 +308,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   p.nA = loki::ceil_div(a->S_max, Lc);
   // A chunks of >= 4096 rows: small GQA parts would make phase-1 items overhead-bound
   p.La = env_int("LOKI_PIPE_LA", Lc >= 4096 ? Lc : 4096);
-  if (p.La < Lc) p.La = Lc;
+  if (p.La < Lc && env_int("LOKI_PIPE_LA", 0) == 0) p.La = Lc;
   if (p.La % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", p.La, p.r1);
   p.nAa = loki::ceil_div(a->S_max, p.La);
   p.units = units;
@@ -348,6 +348,17 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // halves (1) are faster still at one launch (S = 4K 137 -> 125 us, B = 4 73 -> 57) but the tail is a
   // set of units, so shards then agree to rounding only: opt-in
   p.halves = env_int("LOKI_PIPE_HALVES", pl->split ? 0 : ((G >= 2 || g.B <= 4) ? 2 : 0));
+  // few units: smaller A chunks, so phase 1 spreads over the grid -- at least 128 A items for one launch,
+  // one A-launch wave for split layers (r01, tools/la_small.sh: B = 1, S = 4K 39.8 -> 35.4 us; B = 2,
+  // S = 8K 95.7 -> 81.4 us; B = 4, S = 4K keeps 4096-row chunks: 66.8 vs 71.6 us at 1024; GQA B = 1, S = 32K
+  // 209 -> 176 us).  MHA: at most 8 chunks per unit (B = 1, S = 32K: 16 chunks 144 us vs 138 at 4)
+  if (env_int("LOKI_PIPE_LA", 0) == 0) {
+    const long long target = pl->split ? (long long)pl->grid1 : 128;
+    while ((long long)units * p.nAa < target && p.La >= 2048 && (p.La / 2) % p.r1 == 0 && (G > 1 || p.nAa < 8)) {
+      p.La /= 2;
+      p.nAa = loki::ceil_div(a->S_max, p.La);
+    }
+  }
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
   // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn
