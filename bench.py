@@ -572,14 +572,26 @@ def main():
         hv = wl.v_new.cpu().pin_memory()
         hout = torch.empty_like(wl.out[-1], device="cpu").pin_memory()
 
+        # the public serving API: L.DecodeGraph replays the captured layer loop (LokiDecoder.step per layer,
+        # plus the head all-gather when sharded); eager LokiDecoder.step calls if capture is not possible
+        try:
+            dg = L.DecodeGraph(decs, between=(lambda layer: gather_outputs(wl, layer)) if world > 1 else None)
+            run_layers, e2e_path = dg.replay, "paper_2406_02542_b200.DecodeGraph.replay (CUDA graph of LokiDecoder.step per layer; ctypes -> libloki_b200)"
+        except Exception as e:  # pragma: no cover - depends on driver / NCCL build
+            log(f"[bench] DecodeGraph capture failed ({e}); e2e through eager LokiDecoder.step")
+
+            def run_layers():
+                for layer, dec in enumerate(decs):
+                    dec.step()
+                    if world > 1:
+                        gather_outputs(wl, layer)
+            e2e_path = "paper_2406_02542_b200.LokiDecoder.step (ctypes -> libloki_b200), eager launches"
+
         def e2e_step():
             wl.q_raw.copy_(hq, non_blocking=True)
             wl.k_raw.copy_(hk, non_blocking=True)
             wl.v_new.copy_(hv, non_blocking=True)
-            for layer, dec in enumerate(decs):
-                dec.step()
-                if world > 1:
-                    gather_outputs(wl, layer)
+            run_layers()
             hout.copy_(wl.out[-1], non_blocking=True)
         for _ in range(3):
             e2e_step()
@@ -588,7 +600,7 @@ def main():
         bi = (hq.numel() + hk.numel() + hv.numel()) * 4
         e2e = {"value": round(e_ms * 1000.0 / (e_steps * wl.L), 3), "unit": "µs/layer",
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": hout.numel() * 4,
-               "path": "paper_2406_02542_b200.LokiDecoder.step (ctypes -> libloki_b200), eager launches"}
+               "path": e2e_path}
 
     extras = {}
     if not args.no_extras and rank == 0 and world == 1:

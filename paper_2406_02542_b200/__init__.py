@@ -10,6 +10,7 @@ compositions.  The arithmetic runs in hand-written sm_100a CUDA
 __version__ = "0.1.0"
 
 from .attention import (
+    DecodeGraph,
     KvCache,
     LokiConfig,
     LokiDecoder,

@@ -464,3 +464,46 @@ class LokiDecoder:
         self.append(s)
         self.attend(s)
         return self.out
+
+
+class DecodeGraph:
+    """One decode step over a stack of layers -- `LokiDecoder.step` per layer in
+    order, optionally followed by `between(layer)` (e.g. the head all-gather of a
+    sharded layer) -- captured once as a CUDA graph and replayed per token, so the
+    serving loop pays one graph launch instead of ~3 host launches per layer.
+
+    Replays read the decoders' q_raw / k_raw / v_new / rows / lens buffers as they
+    are at replay time (write the next token's inputs into them, then `replay()`).
+    Capture runs the step `warmup` + 1 times on a side stream: like any step, each
+    run writes the new K_hat / V rows at `rows` (the caller advances rows / lens).
+    """
+
+    def __init__(self, decoders, between=None, warmup: int = 2):
+        if not decoders:
+            raise ShapeError("DecodeGraph needs at least one LokiDecoder")
+        self.decoders = list(decoders)
+        self.between = between
+        dev = self.decoders[0].device
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self._run()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._run()
+        torch.cuda.synchronize(dev)
+
+    def _run(self):
+        for layer, dec in enumerate(self.decoders):
+            dec.step()
+            if self.between is not None:
+                self.between(layer)
+
+    def replay(self):
+        """Launch the captured step on the current stream; returns the last layer's output."""
+        self.graph.replay()
+        return self.decoders[-1].out
+

@@ -536,3 +536,37 @@ def test_pipe_geometry_matrix(geom):
                             torch.from_numpy(V).to(DEV, tdt), lens, d=d, k_f=k_f, diagnostics=True)
     ks = [L.resolve_fraction(k_f, s) for s in lens]
     check_sets_and_outputs(q, K, V, lens, d, ks, diag.indices.cpu().numpy(), y.cpu().numpy(), 1e-3)
+
+
+@pytest.mark.gpu
+def test_decode_graph_replay_matches_eager_steps():
+    """DecodeGraph (the serving API: a captured multi-layer step) gives the same
+    bits as eager LokiDecoder.step calls on the same inputs, and follows new
+    inputs written into the decoders' buffers between replays."""
+    B, Hq, Hkv, D, S0, layers = 2, 8, 8, 128, 9000, 3
+    gen = torch.Generator(device=DEV).manual_seed(77)
+    rows = torch.full((B,), S0, dtype=torch.int32, device=DEV)
+    lens = torch.full((B,), S0 + 1, dtype=torch.int32, device=DEV)
+    q_raw = torch.randn(B, Hq, D, device=DEV, generator=gen)
+    k_raw = torch.randn(B, Hkv, D, device=DEV, generator=gen)
+    v_new = torch.randn(B, Hkv, D, device=DEV, generator=gen)
+    decs = []
+    for _ in range(layers):
+        K = torch.randn(B, Hkv, S0 + 1, D, device=DEV, generator=gen).to(torch.bfloat16)
+        V = torch.randn(B, Hkv, S0 + 1, D, device=DEV, generator=gen).to(torch.bfloat16)
+        P = torch.linalg.qr(torch.randn(Hkv, D, D, device=DEV, generator=gen))[0].contiguous()
+        decs.append(L.LokiDecoder(K, V, P, Hq=Hq, d=32, k_f=0.25, rows=rows, lens=lens, S_max=S0 + 1,
+                                  q_raw=q_raw, k_raw=k_raw, v_new=v_new))
+    dg = L.DecodeGraph(decs)
+    for trial in range(2):
+        if trial:
+            q_raw.copy_(torch.randn(B, Hq, D, device=DEV, generator=gen))
+        for dec in decs:
+            dec.step()
+        eager = [dec.out.clone() for dec in decs]
+        for dec in decs:
+            dec.out.zero_()
+        dg.replay()
+        torch.cuda.synchronize()
+        for layer, dec in enumerate(decs):
+            assert torch.equal(dec.out, eager[layer]), (trial, layer)
