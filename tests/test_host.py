@@ -150,3 +150,10 @@ def test_package_never_imports_oracle():
                 "from oracle" not in open(os.path.join(pkg, f)).read(), f
             assert "from oracle" not in open(os.path.join(pkg, f)).read()
             assert "import oracle" not in open(os.path.join(pkg, f)).read()
+
+
+def test_decode_graph_validates_before_capture():
+    """DecodeGraph rejects an empty layer list with the reference's ShapeError
+    before touching the device (capture itself needs a GPU: test_gpu_parity)."""
+    with pytest.raises(L.ShapeError):
+        L.DecodeGraph([])
