@@ -333,8 +333,9 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
     if (occ1 < 1 || occ2 < 1) pl->split = false;
     // A chunks of >= 8192 rows (r01: C2 197.9 -> 193.0 us); the A launch has no lag to feed.  Groups of 8:
     // >= 32768 rows (fewer arrivals into the serial 8-head selection; r01 C5s 3398 -> 3232 us,
-    // tools/c5s_sweep.sh; G = 4 is mixed: C4 -1.3 %, C3 +1.2 %, so it keeps 8192)
-    const int la_min = G_T == 8 ? 32768 : 8192;
+    // tools/c5s_sweep.sh).  Groups of 4: >= 16384 rows once the units alone fill an A wave (C4 877 -> 863 us,
+    // tools/la_big.sh; C3, 256 units, loses 1.2 % with them and keeps 8192)
+    const int la_min = G_T == 8 ? 32768 : (G_T == 4 && units >= sm_count() * occ1 ? 16384 : 8192);
     if (env_int("LOKI_PIPE_LA", 0) == 0 && p.La < la_min) {
       p.La = la_min;
       p.nAa = loki::ceil_div(a->S_max, p.La);
