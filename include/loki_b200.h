@@ -72,7 +72,9 @@ typedef struct loki_decode_args {
   const void* V;           /* value cache                (KvCache.values, attention.py:91-95) */
   loki_kv_geom g;
   const int32_t* lens;     /* [B] device: cached rows per batch, new token included */
-  int32_t S_max;           /* host-side upper bound of lens[] (<= S_cap): sizes the launch */
+  int32_t S_max;           /* upper bound of lens[] (<= S_cap): sizes the launch.  A row whose len
+                              exceeds S_max attends over its first S_max rows only (a replayed graph
+                              keeps its S_max: plan it at S_cap for a cache that grows) */
   int32_t d;               /* ranking columns, 1 <= d <= D (attention.py:176-177) */
   double k_f;              /* k_b = clamp(floor(k_f * len_b + 0.5), 1, len_b) (attention.py:40-46) */
   int32_t k_fixed;         /* > 0: use this k for every row instead (must be <= every len_b) */

@@ -31,12 +31,34 @@ def stream_of(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def as_device(x, dtype=_F32, device=None, keep_dtype=False):
-    """-> (contiguous CUDA tensor, came_from_host)."""
+class _NoGuard:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_GUARD = _NoGuard()
+
+
+def on_device(device):
+    """The library launches on the CURRENT device: make it the tensors' device for the call
+    (a no-op context when it already is, so the steady-state path pays nothing)."""
+    if device.index is None or torch.cuda.current_device() == device.index:
+        return _NO_GUARD
+    return torch.cuda.device(device)
+
+
+def as_device(x, dtype=_F32, device=None, keep_dtype=False, rows_only=False):
+    """-> (contiguous CUDA tensor, came_from_host).  rows_only: a CUDA tensor whose last dim is
+    contiguous is kept as the (possibly strided) view it is -- cache views are never copied."""
     if isinstance(x, torch.Tensor) and x.is_cuda:
         t = x
         if not keep_dtype and t.dtype != dtype:
             t = t.to(dtype)
+        if rows_only and t.dim() >= 1 and t.stride(-1) == 1:
+            return t, False
         return t.contiguous(), False
     dev = device or current_device()
     if isinstance(x, torch.Tensor):
@@ -69,12 +91,37 @@ def cache_dtype_code(t: torch.Tensor) -> int:
     raise UnsupportedShapeError(f"cache dtype {t.dtype} (float32 or bfloat16 only)")
 
 
+def row_capacity(K: torch.Tensor) -> int:
+    """Rows per (b, KV head) of the buffer behind a [B, Hkv, S, D] cache view.
+
+    A prefix view [:, :, :S] of a [B, Hkv, cap, D] buffer (KvCache.storage sliced to its
+    length) is addressed as the buffer itself -- S_cap = cap -- so the kernels see one
+    packed row space and nothing is copied; otherwise S_cap = S."""
+    B, Hkv, S, D = K.shape
+    ss = K.stride(2)
+    if ss < D:
+        return S
+    outer = K.stride(1) if Hkv > 1 else (K.stride(0) if B > 1 else 0)
+    if outer <= S * ss or outer % ss:
+        return S
+    cap = outer // ss
+    if Hkv > 1 and B > 1 and K.stride(0) != Hkv * K.stride(1):
+        return S
+    need = K.storage_offset() + (B * Hkv * cap - 1) * ss + D  # elements the packed view touches
+    if need * K.element_size() > K.untyped_storage().nbytes():
+        return S
+    return cap
+
+
 def geom_of(K: torch.Tensor, Hq: int) -> _lib.KvGeom:
-    """Geometry of a [B, Hkv, S_cap, D] cache view (D contiguous)."""
+    """Geometry of a [B, Hkv, S, D] cache view (D contiguous), S_cap = row_capacity(K)."""
     if K.dim() != 4 or K.stride(3) != 1:
         raise ShapeError(f"cache must be a [B, Hkv, S, D] view with contiguous rows, got {tuple(K.shape)}")
-    B, Hkv, S_cap, D = K.shape
-    return _lib.KvGeom(B, Hq, Hkv, D, S_cap, cache_dtype_code(K), K.stride(0), K.stride(1), K.stride(2))
+    B, Hkv, _, D = K.shape
+    cap = row_capacity(K)
+    sh = K.stride(1) if Hkv > 1 else cap * K.stride(2)
+    sb = K.stride(0) if B > 1 else Hkv * sh
+    return _lib.KvGeom(B, Hq, Hkv, D, cap, cache_dtype_code(K), sb, sh, K.stride(2))
 
 
 @dataclass
@@ -137,7 +184,8 @@ class DecodeCall:
         return {"ctas_per_unit": c.value, "rows_per_cta": r.value, "smem_bytes": s.value}
 
     def run(self, stream=None):
-        _lib.check(self.lib.loki_decode(self._argp, stream if stream is not None else stream_of(self.device)))
+        with on_device(self.device):
+            _lib.check(self.lib.loki_decode(self._argp, stream if stream is not None else stream_of(self.device)))
         return self.outputs
 
 

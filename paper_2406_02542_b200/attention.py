@@ -178,10 +178,11 @@ def _append_call(q_raw, k_raw, v_new, P, inv_freq, rope_mode, cache, positions, 
     if P is not None and P.dim() == 3:
         P_stride = P.stride(0)
     lib = _lib.lib_for(cache.device)
-    _lib.check(lib.loki_append_kv(_lib.ptr(q_raw), _lib.ptr(k_raw), _lib.ptr(v_new), _lib.ptr(P), P_stride,
-                                  _lib.ptr(inv_freq), _lib.ptr(positions), rope_mode, K.data_ptr(), V.data_ptr(),
-                                  geom, cache._rows_tensor().data_ptr(), _lib.ptr(q_hat_out),
-                                  _core.stream_of(cache.device)))
+    with _core.on_device(cache.device):
+        _lib.check(lib.loki_append_kv(_lib.ptr(q_raw), _lib.ptr(k_raw), _lib.ptr(v_new), _lib.ptr(P), P_stride,
+                                      _lib.ptr(inv_freq), _lib.ptr(positions), rope_mode, K.data_ptr(),
+                                      V.data_ptr(), geom, cache._rows_tensor().data_ptr(), _lib.ptr(q_hat_out),
+                                      _core.stream_of(cache.device)))
 
 
 # ------------------------------------------------------------------ validation
@@ -347,26 +348,34 @@ def loki_decode(q_hat, K_hat, V, lens=None, *, d=None, k=None, k_f=None, cfg: Lo
     """Batched Loki decode attention on the device (the north-star hot path).
 
     q_hat [B, Hq, D] fp32 (PCA basis); K_hat / V [B, Hkv, S_cap, D] fp32 or bf16
-    (views of a larger buffer are fine); lens [B] valid rows per batch (default
-    S_cap).  Budget: d and either a fixed k or a fraction k_f (resolved per
+    (row-contiguous views are used in place: a [:, :, :S] slice of a capacity
+    buffer is addressed as that buffer, never copied); lens [B] valid rows per
+    batch (default S_cap).  Budget: d and either a fixed k or a fraction k_f (resolved per
     batch on the device exactly like resolve_fraction), or cfg=LokiConfig.
     Returns y [B, Hq, D] fp32 and, with diagnostics=True, LokiDiagnostics with
     indices int64 [B, Hq, k_max] (-1 past a row's k), approx_scores
     [B, Hq, S_cap] and weights [B, Hq, k_max].
     """
     q, host = _core.as_device(q_hat, torch.float32)
-    K, _ = _core.as_device(K_hat, torch.float32, device=q.device, keep_dtype=True)
-    Vt, _ = _core.as_device(V, torch.float32, device=q.device, keep_dtype=True)
+    K, _ = _core.as_device(K_hat, torch.float32, device=q.device, keep_dtype=True, rows_only=True)
+    Vt, _ = _core.as_device(V, torch.float32, device=q.device, keep_dtype=True, rows_only=True)
     if q.dim() != 3 or K.dim() != 4 or Vt.shape != K.shape:
         raise ShapeError(f"expected q [B, Hq, D] and K, V [B, Hkv, S, D]; got {tuple(q.shape)}, "
                          f"{tuple(K.shape)}, {tuple(Vt.shape)}")
     B, Hq, D = q.shape
     if K.shape[0] != B or K.shape[3] != D or Hq % K.shape[1]:
         raise ShapeError(f"queries {tuple(q.shape)} do not match cache {tuple(K.shape)}")
-    S_cap = K.shape[2]
+    S_cap = K.shape[2]  # the view's rows; the kernels may address a larger buffer behind it (geom_of)
+    if K.stride() != Vt.stride():  # one geometry describes both caches
+        K, Vt = K.contiguous(), Vt.contiguous()
+    phys = _core.row_capacity(K)
     lens_t, lens_h = _core.lens_tensor(S_cap if lens is None else lens, B, q.device)
     if S_max is None:
         S_max = max(lens_h) if lens_h is not None else S_cap
+    if not 1 <= S_max <= S_cap:
+        raise ShapeError(f"S_max {S_max} outside [1, {S_cap}]")
+    if lens_h is not None and max(lens_h) > S_cap:
+        raise ShapeError(f"lens {max(lens_h)} exceed the cache view's {S_cap} rows")
     if lens_h is not None and min(lens_h) < 1:
         raise ShapeError("attention needs at least one cached token")
     if cfg is not None:
@@ -389,7 +398,7 @@ def loki_decode(q_hat, K_hat, V, lens=None, *, d=None, k=None, k_f=None, cfg: Lo
     idx = approx = w = None
     if diagnostics:
         idx = torch.full((B, Hq, kmax), -1, dtype=torch.int32, device=q.device)
-        approx = torch.zeros((B, Hq, S_cap), dtype=torch.float32, device=q.device)
+        approx = torch.zeros((B, Hq, phys), dtype=torch.float32, device=q.device)
         w = torch.zeros((B, Hq, kmax), dtype=torch.float32, device=q.device)
     call = _core.DecodeCall(q, K, Vt, lens_t, S_max, d, k_f=k_f or 0.0, k_fixed=k or 0,
                             select_mode=_lib.SELECT_TOPK, idx_stride=kmax, out=y, idx_out=idx,
@@ -397,7 +406,8 @@ def loki_decode(q_hat, K_hat, V, lens=None, *, d=None, k=None, k_f=None, cfg: Lo
     call.run()
     if not diagnostics:
         return _core.back(y, host)
-    diag = LokiDiagnostics(indices=_core.back(idx.to(torch.int64), host), approx_scores=_core.back(approx, host),
+    diag = LokiDiagnostics(indices=_core.back(idx.to(torch.int64), host),
+                           approx_scores=_core.back(approx[..., :S_cap], host),
                            weights=_core.back(w, host))
     return _core.back(y, host), diag
 
@@ -406,8 +416,10 @@ def dense_decode(q, K, V, lens=None, *, S_max=None, out=None, cluster=0):
     """Batched full attention softmax(K q / sqrt(D)) V (vanilla_attention,
     attention.py:137-142) on the same kernel with every row selected."""
     qq, host = _core.as_device(q, torch.float32)
-    Kt, _ = _core.as_device(K, torch.float32, device=qq.device, keep_dtype=True)
-    Vt, _ = _core.as_device(V, torch.float32, device=qq.device, keep_dtype=True)
+    Kt, _ = _core.as_device(K, torch.float32, device=qq.device, keep_dtype=True, rows_only=True)
+    Vt, _ = _core.as_device(V, torch.float32, device=qq.device, keep_dtype=True, rows_only=True)
+    if Kt.stride() != Vt.stride():
+        Kt, Vt = Kt.contiguous(), Vt.contiguous()
     B, Hq, D = qq.shape
     S_cap = Kt.shape[2]
     lens_t, lens_h = _core.lens_tensor(S_cap if lens is None else lens, B, qq.device)
@@ -425,10 +437,13 @@ class LokiDecoder:
     Holds a KvCache-style storage and runs, per step:
       K0  loki_append_kv: q_raw/k_raw (+RoPE) -> q_hat, K_hat row, V row
       K1-3 loki_decode:   fused approx scores -> top-k -> sparse attention
-    `rows` / `lens` are device int32 [B] tensors owned by the caller.
+    `rows` / `lens` are device int32 [B] tensors owned by the caller.  S_max (default: the
+    cache capacity K.shape[2]) sizes the launch plan and is frozen into a captured graph:
+    a row whose len exceeds it attends over its first S_max rows only, so a serving loop
+    that grows lens between replays keeps the default.
     """
 
-    def __init__(self, K, V, P, *, Hq, d, k_f=None, k=None, rows, lens, S_max, q_raw, k_raw, v_new,
+    def __init__(self, K, V, P, *, Hq, d, k_f=None, k=None, rows, lens, S_max=None, q_raw, k_raw, v_new,
                  rope_mode=_lib.ROPE_NONE, rope_base=10000.0, positions=None, dense=False, out=None, cluster=0):
         self.device = K.device
         self.lib = _lib.lib_for(self.device)
@@ -444,6 +459,9 @@ class LokiDecoder:
         self.P_stride = P.stride(0) if (P is not None and P.dim() == 3) else 0
         self.dense = dense
         self._append_args = None
+        S_max = K.shape[2] if S_max is None else int(S_max)
+        if not 1 <= S_max <= K.shape[2]:
+            raise ShapeError(f"S_max {S_max} outside [1, {K.shape[2]}]")
         self.call = _core.DecodeCall(self.q_hat, K, V, lens, S_max, d, k_f=k_f or 0.0, k_fixed=k or 0,
                                      select_mode=_lib.SELECT_ALL if dense else _lib.SELECT_TOPK, out=self.out,
                                      Hq=Hq, cluster=cluster)
@@ -454,7 +472,8 @@ class LokiDecoder:
                 _lib.ptr(self.q_raw), _lib.ptr(self.k_raw), _lib.ptr(self.v_new), _lib.ptr(self.P), self.P_stride,
                 _lib.ptr(self.inv), _lib.ptr(self.positions), self.rope_mode, self.K.data_ptr(), self.V.data_ptr(),
                 self.geom, self.rows.data_ptr(), self.q_hat.data_ptr())
-        _lib.check(self.lib.loki_append_kv(*self._append_args, stream))
+        with _core.on_device(self.device):
+            _lib.check(self.lib.loki_append_kv(*self._append_args, stream))
 
     def attend(self, stream):
         self.call.run(stream)

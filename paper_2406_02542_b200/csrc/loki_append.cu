@@ -181,11 +181,10 @@ cudaError_t launch_append_t(dim3 grid, size_t smem, cudaStream_t st, const float
                             const int64_t* positions, int rope_mode, void* K, void* V, const loki_kv_geom& g,
                             const int32_t* rows, float* q_hat_out) {
   auto kern = append_kernel<T, P_SMEM>;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static KernelAttrs attrs;
+  {
+    cudaError_t e = attrs.ensure(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    smem_set = smem;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;

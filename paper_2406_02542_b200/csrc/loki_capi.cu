@@ -101,7 +101,15 @@ loki_status validate(const loki_decode_args* a) {
   return LOKI_OK;
 }
 
+// Tuning knobs (LOKI_PIPE_*, LOKI_TMA_*, LOKI_DEBUG, ...) are honoured only with LOKI_TUNING=1, so a
+// deployment's launch plan cannot change silently with its environment.
+bool tuning_enabled() {
+  const char* v = getenv("LOKI_TUNING");
+  return v != nullptr && *v != '\0' && *v != '0';
+}
+
 int env_int(const char* name, int dflt) {
+  if (!tuning_enabled()) return dflt;
   const char* v = getenv(name);
   if (v == nullptr || *v == '\0') return dflt;
   return atoi(v);
@@ -413,6 +421,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   p.D = g.D;
   p.S_cap = g.S_cap;
   p.lens = a->lens;
+  p.S_max = a->S_max;
   p.d = a->d < 1 ? 1 : a->d;
   p.k_f = a->k_f;
   p.k_fixed = a->k_fixed;
@@ -552,6 +561,7 @@ loki_status loki_decode(const loki_decode_args* a, void* stream) {
   p.D = g.D;
   p.S_cap = g.S_cap;
   p.lens = a->lens;
+  p.S_max = a->S_max;
   p.d = a->d < 1 ? 1 : a->d;
   p.k_f = a->k_f;
   p.k_fixed = a->k_fixed;

@@ -5,9 +5,57 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "loki_b200.h"
 
 namespace loki {
+
+// Kernel attributes are per device: a per-device high-water mark of the dynamic
+// shared memory attribute (and the non-portable cluster flag), set under a lock
+// so concurrent callers and several GPUs in one process are safe.  Steady-state
+// launches find the attribute already set and never call into the driver (which
+// also keeps the call out of CUDA-graph capture).
+struct KernelAttrs {
+  static constexpr int kDevs = 64;
+  std::mutex mu;
+  size_t smem[kDevs] = {};
+  bool nonportable[kDevs] = {};
+  cudaError_t ensure(const void* kern, size_t bytes, bool nonportable_cluster = false) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs) dev = kDevs - 1;
+    std::lock_guard<std::mutex> lock(mu);
+    if (bytes > smem[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e != cudaSuccess) return e;
+      smem[dev] = bytes;
+    }
+    if (nonportable_cluster && !nonportable[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      nonportable[dev] = true;
+    }
+    return cudaSuccess;
+  }
+  // resident CTAs per SM at `bytes` of dynamic smem (cached per device: the plan asks on every call)
+  size_t occ_smem[kDevs] = {};
+  int occ[kDevs] = {};
+  int occupancy(const void* kern, int threads, size_t bytes) {
+    if (ensure(kern, bytes) != cudaSuccess) return 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs) dev = kDevs - 1;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (occ_smem[dev] == bytes && occ[dev] > 0) return occ[dev];
+    }
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, bytes) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lock(mu);
+    occ_smem[dev] = bytes;
+    occ[dev] = n;
+    return n;
+  }
+};
 
 constexpr int kWarp = 32;
 

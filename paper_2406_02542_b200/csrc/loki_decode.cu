@@ -220,19 +220,9 @@ static cudaError_t launch_t(const FusedParams& p, int units, size_t smem, cudaSt
   auto kern = fused_decode_kernel<T, G_T, VEC, NCH, NT>;
   // attributes are process-wide per kernel: set them once (also keeps them out
   // of CUDA-graph capture on the steady-state path)
-  static size_t smem_set = 0;
-  static bool nonportable_set = false;
-  cudaError_t e;
-  if (smem > smem_set) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
-  if (p.C > 8 && !nonportable_set) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-    nonportable_set = true;
-  }
+  static KernelAttrs attrs;
+  cudaError_t e = attrs.ensure(reinterpret_cast<const void*>(kern), smem, p.C > 8);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(units * p.C));
   cfg.blockDim = dim3(NT);

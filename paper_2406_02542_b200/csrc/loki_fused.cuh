@@ -119,7 +119,7 @@ __device__ __forceinline__ bool make_ctx(const FusedParams& p, uint8_t* smem, in
   c.D = p.D;
   c.Lmax = p.Lmax;
   int S = p.lens[c.b];
-  S = S > p.S_cap ? p.S_cap : S;
+  S = S > p.S_max ? p.S_max : S;  // S_max <= S_cap (host); slices are sized for S_max rows
   c.S = S;
   if (S <= 0) return false;
   int kb;

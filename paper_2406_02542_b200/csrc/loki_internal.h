@@ -16,7 +16,8 @@ struct FusedParams {
   const void* V;
   int64_t sb, sh, ss;        // element strides (batch, kv head, row)
   int B, Hq, Hkv, G, D, S_cap;
-  const int32_t* lens;       // [B] cache lengths
+  const int32_t* lens;       // [B] cache lengths (clamped to S_max: the plan covers S_max rows per unit)
+  int S_max;
   int d;
   double k_f;
   int k_fixed;
@@ -56,7 +57,8 @@ struct FusedParams {
 struct PipeParams {
   const float* q_hat;  // [B, Hq, D]
   int B, Hq, Hkv, G, D, S_cap;
-  const int32_t* lens;
+  const int32_t* lens;  // [B] cache lengths, clamped to S_max (the ticket space covers S_max rows per unit)
+  int S_max;
   int d;
   double k_f;
   int k_fixed;

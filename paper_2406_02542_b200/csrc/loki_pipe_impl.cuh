@@ -687,7 +687,7 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
   const int nsw = p.nst, SB = p.stage_bytes;
   const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G;
   int S = p.lens[b];
-  S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
+  S = S < 0 ? 0 : (S > p.S_max ? p.S_max : S);  // the ticket space covers S_max <= S_cap rows
   const int nparts = ceil_div(S > 0 ? S : 1, p.La);
   if (c >= nparts) return 0;  // past this unit's length: not an arrival
   const int row0 = c * p.La;
@@ -1311,7 +1311,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   const int nsw = p.nst, SB = p.stage_bytes;
   const int b = u / p.Hkv, hk = u % p.Hkv, G = p.G, D = D_T;
   int S = p.lens[b];
-  S = S < 0 ? 0 : (S > p.S_cap ? p.S_cap : S);
+  S = S < 0 ? 0 : (S > p.S_max ? p.S_max : S);  // the ticket space covers S_max <= S_cap rows
   const int nparts = ceil_div(S > 0 ? S : 1, p.Lc);
   if (q >= nparts) return 0;  // past this unit's length: not an arrival
   // full part q = rows [q Lc, (q + 1) Lc); the tail units' half parts (half = 0 / 1) cover Lc / 2 rows each
@@ -1617,14 +1617,18 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
 }  // namespace
 
 
+template <typename T, int G_T, int VEC, int D_T, bool BIG, int MODE>
+KernelAttrs& pipe_attrs() {  // one per instantiation, shared by the launch and the occupancy query
+  static KernelAttrs a;
+  return a;
+}
+
 template <typename T, int G_T, int VEC, int D_T, bool BIG, int MODE = 0>
 inline cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st) {
   auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG, MODE>;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = pipe_attrs<T, G_T, VEC, D_T, BIG, MODE>().ensure(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    smem_set = smem;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -1643,10 +1647,7 @@ inline cudaError_t launch_pipe_t(const PipeParams& p, int grid, size_t smem, con
 template <typename T, int G_T, int VEC, int D_T, bool BIG, int MODE = 0>
 inline int occupancy_t(size_t smem) {
   auto kern = pipe_decode_kernel<T, G_T, VEC, D_T, BIG, MODE>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kPT, smem) != cudaSuccess) return 0;
-  return n;
+  return pipe_attrs<T, G_T, VEC, D_T, BIG, MODE>().occupancy(reinterpret_cast<const void*>(kern), kPT, smem);
 }
 
 

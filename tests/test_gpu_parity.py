@@ -469,6 +469,7 @@ def _topk_of(q_hat, Kt, Vt, S, k):
 def test_pipe_variants_match_oracle(env, monkeypatch):
     """The pipe kernel's opt-in variants (split-K tensor-core phase 3, 8192-row chunks, speculative
     boundary candidates, large A chunks) and the cluster kernel give the same parity on MHA and GQA."""
+    monkeypatch.setenv("LOKI_TUNING", "1")  # tuning knobs are ignored without it
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for B, Hq, Hkv, S in [(2, 2, 2, 8192), (2, 4, 1, 5000)]:

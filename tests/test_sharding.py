@@ -87,6 +87,7 @@ def test_sharded_decode_bit_identical_on_gpu(monkeypatch, halves, B, Hq, Hkv):
     import paper_2406_02542_b200 as L
 
     if halves is not None:
+        monkeypatch.setenv("LOKI_TUNING", "1")
         monkeypatch.setenv("LOKI_PIPE_HALVES", halves)
     dev = torch.device("cuda", 0)
     D, S = 128, 4096

@@ -13,6 +13,7 @@ import sys
 
 import torch
 
+os.environ.setdefault("LOKI_TUNING", "1")  # honour LOKI_* tuning knobs (ignored by the library otherwise)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2406_02542_b200 as L  # noqa: E402
 from paper_2406_02542_b200 import _core, _lib  # noqa: E402
