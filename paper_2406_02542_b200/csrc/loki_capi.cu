@@ -167,13 +167,11 @@ loki_status make_plan(const loki_decode_args* a, loki::Plan* plan, loki::FusedPa
                (g.stride_b % vec == 0) && (a->K == nullptr || aligned(a->K, vbytes)) &&
                (a->V == nullptr || aligned(a->V, vbytes));
 
-  // TMA path: cache reachable as one 2-D [B*Hkv*S_cap, D] row space, 16 B aligned
-  const bool contiguous = (g.Hkv == 1 || g.stride_h == (int64_t)g.S_cap * g.stride_s) &&
-                          (g.B == 1 || g.stride_b == (int64_t)g.Hkv * g.S_cap * g.stride_s);
+  // TMA path: cache reachable as one 2-D [rows, D] row space (any whole-row head / batch strides), 16 B aligned
+  const loki::RowSpace rs = loki::row_space(g);
   plan->tma = env_int("LOKI_TMA", 1) != 0 && a->K != nullptr && a->V != nullptr && a->ext_scores == nullptr &&
-              contiguous && aligned(a->K, 16) && aligned(a->V, 16) && (g.stride_s * ebytes) % 16 == 0 &&
-              (long long)g.B * g.Hkv * g.S_cap < (1LL << 31) && loki::tma_supported(g.dtype, g.D, plan->G_T) &&
-              tma_geom(a, plan->G_T, tg);
+              rs.ok && aligned(a->K, 16) && aligned(a->V, 16) && (g.stride_s * ebytes) % 16 == 0 &&
+              loki::tma_supported(g.dtype, g.D, plan->G_T) && tma_geom(a, plan->G_T, tg);
   const int kStageBytes = stage_bytes_cfg();
   const int NTt = loki::kTmaThreads;
   const int align = plan->tma ? tg->r1 : 1;
@@ -234,7 +232,8 @@ loki_status make_plan(const loki_decode_args* a, loki::Plan* plan, loki::FusedPa
     p->r1 = tg->r1;
     p->dbox = tg->dbox;
     p->r3 = tg->r3;
-    p->unit_rows = g.S_cap;
+    p->row_sb = rs.sb;
+    p->row_sh = rs.sh;
   }
   return LOKI_OK;
 }
@@ -247,11 +246,14 @@ struct PipePlan {
   int G_T = 1;
   bool big = false;
   bool split = false;  // A-only launch + B-only launch (MHA bf16)
+  bool ws_select = false;  // the A launch is the warp-specialised pipe_select_kernel (layout in sel_layout)
+  loki::PipeParams sel_layout{};
   int grid = 0, grid1 = 0, grid2 = 0;
   size_t smem1 = 0;
   size_t smem = 0;
   size_t ws = 0;
   size_t off_hist = 0, off_keys = 0, off_tcs = 0, off_poff = 0, off_part = 0, off_spec = 0, off_logits = 0;
+  size_t off_loff = 0;
 };
 
 // The persistent pipelined kernel (loki_pipe.cu) serves the attending TOPK
@@ -260,11 +262,10 @@ bool pipe_eligible(const loki_decode_args* a) {
   const loki_kv_geom& g = a->g;
   const int G_T = loki::next_pow2(g.Hq / g.Hkv);
   const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
-  const bool contiguous = (g.Hkv == 1 || g.stride_h == (int64_t)g.S_cap * g.stride_s) &&
-                          (g.B == 1 || g.stride_b == (int64_t)g.Hkv * g.S_cap * g.stride_s);
+  const loki::RowSpace rs = loki::row_space(g);
   return env_int("LOKI_PIPE", 1) != 0 && a->select_mode == LOKI_SELECT_TOPK && a->ext_scores == nullptr &&
-         a->out != nullptr && a->K != nullptr && a->V != nullptr && contiguous && aligned(a->K, 16) &&
-         aligned(a->V, 16) && (g.stride_s * e) % 16 == 0 && (long long)g.B * g.Hkv * g.S_cap < (1LL << 31) &&
+         a->out != nullptr && a->K != nullptr && a->V != nullptr && rs.ok && aligned(a->K, 16) &&
+         aligned(a->V, 16) && (g.stride_s * e) % 16 == 0 &&
          a->S_max < (1 << 24) && loki::pipe_supported(g.dtype, g.D, G_T) && a->cluster_override == 0;
 }
 
@@ -371,6 +372,34 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
       p.nAa = loki::ceil_div(a->S_max, p.La);
     }
   }
+  // lists mode: single-chunk units select on chip and publish ordered entry lists (no global keys, no
+  // histogram merge, no L2 key re-stream; B items copy their slice).  Needs the unit's keys on chip next
+  // to the ring: the A-only launch of a split layer carries them in place of the B-entry region
+  p.lists = 0;
+  const size_t kchip = (size_t)G_T * p.La * 4;
+  if (pl->split && G_T == 1 && !pl->big && env_int("LOKI_LISTS", 1) != 0 && p.nAa == 1 && !p.spec && !p.split_k &&
+      a->idx_out == nullptr && a->weights_out == nullptr && ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0 && p.Lc / 2 >= 4) {
+    // preferred: the warp-specialised A launch (stream group + select group, one 16-warp CTA per SM)
+    loki::PipeParams ps = p;
+    const size_t sw = loki::pipe_select_layout(&ps);
+    const int ow = (p.lead_swz == 64 || p.lead_swz == 128) && env_int("LOKI_SELECT_WS", 1) != 0
+                       ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, sw) : 0;
+    const size_t s1 = (size_t)p.off_ents + kchip + 1024;
+    const int o1 = ow >= 1 ? 0 : loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, s1, pl->big, 3);
+    if (sw <= kSmemMax && ow >= 1) {
+      p.lists = 1;
+      pl->ws_select = true;
+      pl->sel_layout = ps;
+      pl->smem1 = sw;
+      pl->grid1 = sm_count() * ow;
+    } else if (s1 <= kSmemMax && o1 >= 1) {  // MODE 3: the A-only launch carries the keys in place of the B entries
+      p.lists = 1;
+      p.off_kchip = p.off_ents;
+      pl->smem1 = s1;
+      const int a_ctas = env_int("LOKI_PIPE_A_CTAS", o1);
+      pl->grid1 = sm_count() * (a_ctas < o1 ? (a_ctas < 1 ? 1 : a_ctas) : o1);
+    }
+  }
   const int per_sm = env_int("LOKI_PIPE_CTAS_PER_SM", occ);
   pl->grid = sm_count() * (per_sm < occ ? (per_sm < 1 ? 1 : per_sm) : occ);
   // B tickets trail A tickets by enough work to cover a unit's selection, which walks the G heads in turn
@@ -403,6 +432,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   }
   pl->off_logits = off;
   if (a->weights_out != nullptr) off = loki::align_up(off + (size_t)units * G * g.S_cap * 4, 256);
+  pl->off_loff = off;
+  if (p.lists) off = loki::align_up(off + (size_t)units * (2 * p.nA + 1) * 4, 256);
   pl->ws = off;
   return LOKI_OK;
 }
@@ -431,7 +462,11 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   p.approx_out = a->approx_out;
   p.weights_out = a->weights_out;
   p.qscale = (float)(1.4426950408889634 / sqrt((double)g.D));
-  p.unit_rows = g.S_cap;
+  {
+    const loki::RowSpace rs = loki::row_space(g);
+    p.row_sb = rs.sb;
+    p.row_sh = rs.sh;
+  }
   p.ctrl = reinterpret_cast<uint32_t*>(ws);
   p.hist = reinterpret_cast<uint32_t*>(ws + pl.off_hist);
   p.keys = reinterpret_cast<uint32_t*>(ws + pl.off_keys);
@@ -447,7 +482,10 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   }
   p.part = reinterpret_cast<float*>(ws + pl.off_part);
   p.logits = a->weights_out ? reinterpret_cast<float*>(ws + pl.off_logits) : nullptr;
+  p.sel = p.lists ? p.keys : nullptr;
+  p.loff = p.lists ? reinterpret_cast<uint32_t*>(ws + pl.off_loff) : nullptr;
   p.debug = env_int("LOKI_DEBUG", 0);
+  p.spin_ns = (long long)env_int("LOKI_SPIN_S", 20) * 1000000000LL;  // sanitizer runs raise it
   p.trace = (loki::g_phase_trace != nullptr && p.n_tickets * 4 <= (long long)loki::g_phase_trace_ctas * 8)
                 ? loki::g_phase_trace : nullptr;
   loki::TmaDesc maps[4];
@@ -456,7 +494,6 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   cudaError_t e;
   if (pl.split) {
     loki::PipeParams pa = p, pb = p;
-    pa.trace = pb.trace = nullptr;
     pa.n_tickets = (long long)p.units * p.nAa;
     // units whose B parts run as halves (short drain, opt-in: the grouping of the partial states then
     // depends on the number of units, so KV-head shards would not be bit-identical to one launch)
@@ -464,7 +501,23 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
                : p.halves ? (int)ceil(env_int("LOKI_PIPE_TAIL_X10", 2) / 10.0 * pl.grid2 / p.nA) : 0;
     pb.lag = tail > p.units ? p.units : tail;
     pb.n_tickets = (long long)(p.units - pb.lag) * p.nA + (long long)pb.lag * 2 * p.nA;
-    e = loki::launch_pipe(pa, g.dtype, pl.G_T, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big, 1);
+    // trace rows: the A launch's tickets, then the B launch's (diagnostics only)
+    const bool fits = loki::g_phase_trace != nullptr &&
+                      (pa.n_tickets + pb.n_tickets) * 4 <= (long long)loki::g_phase_trace_ctas * 8;
+    pa.trace = fits ? loki::g_phase_trace : nullptr;
+    pb.trace = fits ? loki::g_phase_trace + pa.n_tickets * 4 : nullptr;
+    if (pl.ws_select) {
+      pa.off_ring = pl.sel_layout.off_ring;
+      pa.off_bars = pl.sel_layout.off_bars;
+      pa.off_hist = pl.sel_layout.off_hist;
+      pa.off_kchip = pl.sel_layout.off_kchip;
+      pa.off_cand = pl.sel_layout.off_cand;
+      pa.cand_bytes = pl.sel_layout.cand_bytes;
+      e = loki::launch_pipe_select(pa, g.dtype, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream));
+    } else {
+      e = loki::launch_pipe(pa, g.dtype, pl.G_T, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big,
+                            p.lists ? 3 : 1);
+    }
     if (e == cudaSuccess)
       e = loki::launch_pipe(pb, g.dtype, pl.G_T, pl.grid2, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big, 2);
   } else {

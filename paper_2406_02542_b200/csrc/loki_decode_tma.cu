@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(NW * 32) fused_decode_tma_kernel(
   const unsigned stage_bytes = (unsigned)(2 * R3 * ROWB);
   const bool want_logits = p.weights_out != nullptr;
   const bool gather = !c.select_all || (p.debug & 1);
-  const int row_base = (int)(((long long)c.b * p.Hkv + c.hk) * p.unit_rows) + c.s0;
+  const int row_base = (int)((long long)c.b * p.row_sb + (long long)c.hk * p.row_sh) + c.s0;
   const int mine = nstage > w ? ceil_div(nstage - w, NW) : 0;  // stages w, w + NW, ...
   // all lanes call issue (the row indices are spread over the lanes); lane 0 issues
   auto issue = [&](int k, const RingPos& at) {
@@ -362,7 +362,7 @@ bool encode_rows(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_k
   const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   const CUtensorMapDataType dt =
       g.dtype == LOKI_DTYPE_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  cuuint64_t dims[2] = {(cuuint64_t)g.D, (cuuint64_t)g.B * g.Hkv * g.S_cap};
+  cuuint64_t dims[2] = {(cuuint64_t)g.D, (cuuint64_t)row_space(g).total};
   cuuint64_t str[1] = {(cuuint64_t)(g.stride_s * e)};
   cuuint32_t box[2] = {(cuuint32_t)(width > 0 ? width : g.D), 1};
   cuuint32_t es[2] = {1, 1};
@@ -374,6 +374,20 @@ bool encode_rows(EncodeTiledFn enc, TmaDesc* out, const void* base, const loki_k
 }
 
 }  // namespace
+
+RowSpace row_space(const loki_kv_geom& g) {
+  RowSpace r;
+  const long long ss = g.stride_s;
+  // size-1 dimensions may carry any stride in a torch view: give them the packed one
+  const long long sh = g.Hkv == 1 ? (long long)g.S_cap * ss : (long long)g.stride_h;
+  const long long sb = g.B == 1 ? (long long)g.Hkv * sh : (long long)g.stride_b;
+  if (ss < g.D || sh % ss != 0 || sb % ss != 0 || sh < (long long)g.S_cap * ss || sb < 0) return r;
+  r.sh = sh / ss;
+  r.sb = sb / ss;
+  r.total = (long long)(g.B - 1) * r.sb + (long long)(g.Hkv - 1) * r.sh + g.S_cap;
+  r.ok = r.total < (1LL << 31);
+  return r;
+}
 
 bool encode_tma(const void* K, const void* V, const loki_kv_geom& g, int dbox, int r1, int r3, TmaDesc* maps) {
   EncodeTiledFn enc = encode_fn();

@@ -39,7 +39,7 @@ struct FusedParams {
   int nst, stage_bytes, off_ring, off_bars;
   int r1, dbox;              // phase-1 box: r1 rows x dbox leading columns
   int r3;                    // phase-3 stage: r3 gathered rows of K and of V
-  long long unit_rows;       // rows per (b, kv head) in the 2-D gather view (= S_cap)
+  long long row_sb, row_sh;  // the 2-D gather view: row of (b, kv head, s) = b * row_sb + h * row_sh + s
   long long* trace;          // optional [grid][8] %globaltimer stamps at phase boundaries
   int debug;                 // LOKI_DEBUG bits (tuning experiments only): 1 = dense rows via gather4
 };
@@ -70,7 +70,7 @@ struct PipeParams {
   float qscale;  // log2(e) / sqrt(D)
   int nst, stage_bytes, off_ring, off_bars, off_hist, off_ents;
   int r1, dbox, r3;
-  long long unit_rows;
+  long long row_sb, row_sh;  // the 2-D gather view: row of (b, kv head, s) = b * row_sb + h * row_sh + s
   int units, Lc, nA, lag, hbits, cand_cap;  // Lc / nA: B-part rows / B parts per unit
   int La, nAa;       // A-chunk rows / A chunks per unit (La >= Lc: phase-1 items are not overhead-bound)
   long long n_tickets;
@@ -92,7 +92,17 @@ struct PipeParams {
   uint32_t* cwin;    // [units][G][nA] each chunk's bin window lo | hi << 16
   long long* trace;  // optional [n_tickets][4] {start, end, sm | kind << 16 | block << 32, tail start}
   int debug;
-  int halves;        // B parts in halves: 2 every unit, 1 tail units only (grouping then depends on #units), 0 none
+  int halves;
+  // lists mode (single-chunk units): the A item keeps the unit's keys on chip ([G][La] words at
+  // off_kchip), selects there and publishes the ordered entries (head mask << 24 | row) of every
+  // selected row to sel[u] plus each half part's entry offset to loff[u][0 .. 2 nA]; B items copy
+  // their slice instead of re-deriving it from the keys
+  int lists;
+  int off_kchip;
+  int off_cand, cand_bytes;  // warp-specialised A launch: the select group's candidate buffers
+  long long spin_ns;  // B items trap after waiting this long for their unit's selection (0: never)
+  uint32_t* sel;     // [units][kstride] (aliases keys: lists mode writes no global keys)
+  uint32_t* loff;    // [units][2 nA + 1]        // B parts in halves: 2 every unit, 1 tail units only (grouping then depends on #units), 0 none
 };
 
 // Phase-trace buffer installed by loki_set_phase_trace (diagnostics only).
@@ -110,6 +120,15 @@ struct Plan {
   size_t workspace = 0;
   int dtype = LOKI_DTYPE_F32;
 };
+
+// The cache as one 2-D [rows, D] row space for TMA row gathers: row of (b, h, s)
+// = b * sb + h * sh + s.  ok == false when the strides are not whole rows or the
+// space needs more than 2^31 rows (then the LDG kernels serve the call).
+struct RowSpace {
+  long long sb = 0, sh = 0, total = 0;
+  bool ok = false;
+};
+RowSpace row_space(const loki_kv_geom& g);
 
 // Opaque 128-byte TMA descriptors (CUtensorMap) built on the host.
 struct alignas(64) TmaDesc {
@@ -161,6 +180,12 @@ bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int db
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
                         cudaStream_t st, bool big, int mode = 0);
 int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode = 0);
+// warp-specialised A launch of lists-mode split layers (MHA bf16, lead rows of 64 / 128 B): sets the
+// layout offsets in *p (ring, bars, double-buffered histograms and keys, candidates) and returns its bytes
+size_t pipe_select_layout(PipeParams* p);
+int pipe_select_ctas_per_sm(int dtype, int lead_rb, size_t smem);
+cudaError_t launch_pipe_select(const PipeParams& p, int dtype, int grid, size_t smem, const TmaDesc* maps,
+                               cudaStream_t st);
 int pipe_warps();
 // 128-row blocks per warp in a B part (Lc = blocks * 128 * warps), shared by kernel and host
 __host__ __device__ constexpr int pipe_blocks_per_warp(int G_T, bool big) {

@@ -67,6 +67,24 @@ struct PipeShared {
   float gm[kMaxG], gl[kMaxG];
 };
 
+// Thread groups the selection helpers run on: the whole CTA, or a warp group of
+// a warp-specialised CTA (its own named barrier; the other group keeps going).
+struct CtaGroup {
+  static constexpr int kThreads = kPT, kWarps = kPW;
+  __device__ __forceinline__ static int tid() { return threadIdx.x; }
+  __device__ __forceinline__ static int warp() { return threadIdx.x >> 5; }
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+template <int FIRST_WARP, int NWARPS, int BAR_ID>
+struct WarpGroup {
+  static constexpr int kThreads = NWARPS * 32, kWarps = NWARPS;
+  __device__ __forceinline__ static int tid() { return (int)threadIdx.x - FIRST_WARP * 32; }
+  __device__ __forceinline__ static int warp() { return ((int)threadIdx.x >> 5) - FIRST_WARP; }
+  __device__ __forceinline__ static void sync() {
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR_ID), "n"(NWARPS * 32) : "memory");
+  }
+};
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -118,9 +136,10 @@ __device__ __forceinline__ int k_of(const PipeParams& p, int S) {
   return p.k_fixed > 0 ? (p.k_fixed < S ? p.k_fixed : S) : resolve_fraction(p.k_f, S);
 }
 
-// Block-wide inclusive scan of one value per thread, in thread order.
+// Group-wide inclusive scan of one value per thread, in thread order.
+template <typename Grp = CtaGroup>
 __device__ __forceinline__ unsigned block_incl_scan(unsigned v, PipeShared& sh, unsigned* total) {
-  const int lane = lane_id(), w = warp_id();
+  const int lane = lane_id(), w = Grp::warp();
   unsigned x = v;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -128,30 +147,31 @@ __device__ __forceinline__ unsigned block_incl_scan(unsigned v, PipeShared& sh, 
     if (lane >= off) x += t;
   }
   if (lane == 31) sh.scan[w] = (int)x;
-  __syncthreads();
+  Grp::sync();
   unsigned before = 0, tot = 0;
 #pragma unroll
-  for (int i = 0; i < kPW; ++i) {
+  for (int i = 0; i < Grp::kWarps; ++i) {
     const unsigned c = (unsigned)sh.scan[i];
     before += i < w ? c : 0u;
     tot += c;
   }
-  __syncthreads();
+  Grp::sync();
   *total = tot;
   return before + x;
 }
 
 // The bin holding the need-th largest element: largest b with
 // sum_{i>b} h[i] < need <= sum_{i>=b} h[i] -> sh.fb_bin / fb_above / fb_cnt.
+template <typename Grp = CtaGroup>
 __device__ void find_bin(const uint32_t* h, int nbins, unsigned need, PipeShared& sh) {
-  const int tid = threadIdx.x;
-  const int per = nbins > kPT ? nbins / kPT : 1;  // nbins is a power of two
-  const int hi = nbins - tid * per;                // this thread owns bins [hi - per, hi)
+  const int tid = Grp::tid();
+  const int per = nbins > Grp::kThreads ? nbins / Grp::kThreads : 1;  // nbins is a power of two
+  const int hi = nbins - tid * per;                                    // this thread owns bins [hi - per, hi)
   unsigned s = 0;
   if (hi > 0)
     for (int i = 0; i < per; ++i) s += h[hi - 1 - i];
   unsigned tot;
-  const unsigned incl = block_incl_scan(s, sh, &tot);
+  const unsigned incl = block_incl_scan<Grp>(s, sh, &tot);
   const unsigned excl = incl - s;
   if (hi > 0 && excl < need && need <= incl) {
     unsigned acc = excl;
@@ -166,7 +186,7 @@ __device__ void find_bin(const uint32_t* h, int nbins, unsigned need, PipeShared
       acc += h[b];
     }
   }
-  __syncthreads();
+  Grp::sync();
 }
 
 // Warp-aggregated append of `c` to dst when `m` (order within dst is irrelevant).
@@ -262,8 +282,9 @@ struct KeyStream {
 };
 
 // LOKI_DEBUG & 16 (tuning only): %globaltimer at selection checkpoints, [units][8] at trace + 2^21
+template <typename Grp = CtaGroup>
 __device__ __forceinline__ void sel_stamp(const PipeParams& p, int u, int k) {
-  if ((p.debug & 16) && p.trace != nullptr && threadIdx.x == 0) p.trace[(1 << 21) + (size_t)u * 8 + k] = globaltimer();
+  if ((p.debug & 16) && p.trace != nullptr && Grp::tid() == 0) p.trace[(1 << 21) + (size_t)u * 8 + k] = globaltimer();
 }
 
 // Threshold of each head's top-k in unit u on 64-bit composite keys: the
@@ -521,11 +542,203 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
   sel_stamp(p, u, 6);
 }
 
+// Selection of a single-chunk unit with everything on chip: the unit's keys
+// ([G][kst] in shared memory) and its complete level-0 histogram are where the
+// A item left them, so the threshold costs no L2 round trip.  Same composite-key
+// rule as select_unit (linalg.py:95-118): the boundary bin's rows are compacted
+// into `scratch` (the idle TMA ring) when they fit, else narrowed by further
+// histogram levels over the on-chip keys; radix passes over the candidates, then
+// a direct rank once <= 256 remain.  Thresholds -> sh.Tc[g].
+template <int G_T, typename Grp = CtaGroup>
+__device__ void select_onchip(const PipeParams& p, int u, int S, const uint32_t* ks, int kst, uint32_t* hist,
+                              uint8_t* scratch, int scratch_bytes, PipeShared& sh) {
+  const int tid = Grp::tid();
+  const int G = p.G, hb = p.hbits, HB = 1 << hb;
+  const int kb = k_of(p, S);
+  const int cap = scratch_bytes / 16;
+  unsigned long long* candA = reinterpret_cast<unsigned long long*>(scratch);
+  unsigned long long* candB = candA + cap;
+  for (int g = 0; g < G; ++g) {
+    const uint32_t* kg = ks + (size_t)g * kst;
+    uint32_t* h = hist + g * HB;  // consumed by find_bin, then reused for deeper levels
+    if (kb <= 0 || kb >= S) {     // nothing / everything selected
+      if (tid == 0) sh.Tc[g] = kb <= 0 ? ~0ull : 0ull;
+      continue;
+    }
+    find_bin<Grp>(h, HB, (unsigned)kb, sh);
+    if (g == 0) sel_stamp<Grp>(p, u, 1);
+    unsigned long long P = (unsigned long long)sh.fb_bin;
+    int nb = hb;
+    unsigned need = (unsigned)kb - sh.fb_above, cnt = sh.fb_cnt;
+    int ncand = 0;
+    bool listed = false;
+    for (;;) {
+      if (cnt == need) break;  // the whole boundary prefix is selected
+      const int sh64 = 64 - nb;
+      if (cnt <= (unsigned)cap) {  // compact the rows matching P
+        if (tid == 0) sh.ncand = 0;
+        Grp::sync();
+        const int lane = lane_id();
+        for (int i0 = 0; i0 < S; i0 += 4 * Grp::kThreads) {
+          const int il = i0 + 4 * tid;
+          uint4 kk = make_uint4(0u, 0u, 0u, 0u);
+          if (il < S) kk = *reinterpret_cast<const uint4*>(kg + il);  // kst % 4 == 0, rows past S masked
+          unsigned hit = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            hit |= (il + e < S && (comp_key(u4_at(kk, e), il + e) >> sh64) == P ? 1u : 0u) << e;
+          if (__any_sync(0xffffffffu, hit != 0u)) {  // one shared atomic per warp, then ordered-free writes
+            int tot;
+            const int ex = warp_excl_scan(__popc(hit), &tot);
+            int at = 0;
+            if (lane == 0) at = atomicAdd(&sh.ncand, tot);
+            at = __shfl_sync(0xffffffffu, at, 0) + ex;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if ((hit >> e) & 1u) candA[at++] = comp_key(u4_at(kk, e), il + e);
+          }
+        }
+        Grp::sync();
+        ncand = sh.ncand;
+        listed = true;
+        break;
+      }
+      // one more histogram level over the rows matching P
+      const int bits = min(hb, 64 - nb);
+      for (int i = tid; i < (1 << bits); i += Grp::kThreads) h[i] = 0u;
+      Grp::sync();
+      for (int i = tid; i < S; i += Grp::kThreads) {
+        const unsigned long long c = comp_key(kg[i], i);
+        if ((c >> sh64) == P) atomicAdd(&h[(c >> (sh64 - bits)) & ((1ull << bits) - 1)], 1u);
+      }
+      Grp::sync();
+      find_bin<Grp>(h, 1 << bits, need, sh);
+      P = (P << bits) | (unsigned long long)sh.fb_bin;
+      nb += bits;
+      need -= sh.fb_above;
+      cnt = sh.fb_cnt;
+    }
+    unsigned long long Tc = nb >= 64 ? P : (P << (64 - nb));
+    if (g == 0) sel_stamp<Grp>(p, u, 2);
+    if ((p.debug & 16) && p.trace != nullptr && tid == 0 && g == 0) p.trace[(1 << 21) + (size_t)u * 8 + 7] = ncand;
+    if (listed && cnt != need) {
+      const unsigned long long* src = candA;
+      unsigned long long* dst = candB;
+      while (ncand > 32) {
+        const int bits = min(8, 64 - nb);
+        for (int i = tid; i < (1 << bits); i += Grp::kThreads) h[i] = 0u;
+        Grp::sync();
+        for (int i = tid; i < ncand; i += Grp::kThreads) atomicAdd(&h[(src[i] >> (64 - nb - bits)) & ((1ull << bits) - 1)], 1u);
+        Grp::sync();
+        find_bin<Grp>(h, 1 << bits, need, sh);
+        P = (P << bits) | (unsigned long long)sh.fb_bin;
+        nb += bits;
+        need -= sh.fb_above;
+        cnt = sh.fb_cnt;
+        if (cnt == need) break;
+        if (tid == 0) sh.ncand = 0;
+        Grp::sync();
+        for (int i0 = 0; i0 < ncand; i0 += Grp::kThreads) {
+          const int i = i0 + tid;
+          const unsigned long long c = i < ncand ? src[i] : 0ull;
+          append_if(i < ncand && (c >> (64 - nb)) == P, c, dst, &sh.ncand);
+        }
+        Grp::sync();
+        ncand = sh.ncand;
+        unsigned long long* was = const_cast<unsigned long long*>(src);
+        src = dst;
+        dst = was;
+      }
+      if (cnt == need) {
+        Tc = nb >= 64 ? P : (P << (64 - nb));
+      } else {  // <= 32 distinct candidates, one per lane of warp 0: the need-th largest by rank
+        if (tid < 32) {
+          const unsigned long long c = tid < ncand ? src[tid] : 0ull;
+          unsigned rank = 0;
+          for (int i = 0; i < ncand; ++i) rank += __shfl_sync(0xffffffffu, c, i) > c;
+          if (tid < ncand && rank == need - 1) sh.tsel = c;
+        }
+        Grp::sync();
+        Tc = sh.tsel;
+      }
+    }
+    if (g == 0) sel_stamp<Grp>(p, u, 3);
+    if (tid == 0) sh.Tc[g] = Tc;
+    Grp::sync();
+  }
+  Grp::sync();
+}
+
+// Ordered emission of a single-chunk unit's selection: entries (head mask << 24
+// | row) of every row some head of the group selected, ascending, to p.sel[u],
+// plus the entry offset of every half part (Lc / 2 rows) to p.loff[u] -- the B
+// items read their part's slice instead of re-deriving it from the keys.  Warp w
+// owns the contiguous rows [w S8, (w + 1) S8): a counting pass (ballots), one
+// block exclusive scan of the warp totals, then an ordered writing pass.
+template <int G_T, typename Grp = CtaGroup>
+__device__ void emit_lists(const PipeParams& p, int u, int S, const uint32_t* ks, int kst, PipeShared& sh) {
+  const int lane = lane_id(), w = Grp::warp();
+  const int G = p.G;
+  const int lhs = 31 - __clz(p.Lc / 2);  // Lc / 2 is a power of two
+  uint32_t* dst = p.sel + (size_t)u * p.kstride;
+  uint32_t* lo = p.loff + (size_t)u * (2 * p.nA + 1);
+  unsigned long long Tc[G_T];
+#pragma unroll
+  for (int g = 0; g < G_T; ++g) Tc[g] = g < G ? sh.Tc[g] : ~0ull;
+  // warp w: rows [r0, r1), 128 per pass (4 per lane, one uint4 of keys per head)
+  const int S8 = ceil_div(ceil_div(S > 0 ? S : 1, Grp::kWarps), 128) * 128;
+  const int r0 = min(S, w * S8), r1 = min(S, r0 + S8);
+  auto masks = [&](int j, unsigned (&m)[4]) -> int {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m[e] = 0u;
+    if (j < r1) {
+#pragma unroll
+      for (int g = 0; g < G_T; ++g) {
+        if (g < G) {
+          const uint4 kk = *reinterpret_cast<const uint4*>(ks + (size_t)g * kst + j);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            m[e] |= (j + e < r1 && comp_key(u4_at(kk, e), j + e) >= Tc[g] ? 1u : 0u) << g;
+        }
+      }
+    }
+    return (m[0] != 0u) + (m[1] != 0u) + (m[2] != 0u) + (m[3] != 0u);
+  };
+  unsigned cnt = 0;
+  for (int j0 = r0; j0 < r1; j0 += 128) {
+    unsigned m[4];
+    cnt += __reduce_add_sync(0xffffffffu, (unsigned)masks(j0 + 4 * lane, m));
+  }
+  if (lane == 0) sh.scan[w] = (int)cnt;
+  Grp::sync();
+  unsigned base = 0, total = 0;
+#pragma unroll
+  for (int i = 0; i < Grp::kWarps; ++i) {
+    base += i < w ? (unsigned)sh.scan[i] : 0u;
+    total += (unsigned)sh.scan[i];
+  }
+  for (int j0 = r0; j0 < r1; j0 += 128) {
+    const int j = j0 + 4 * lane;
+    unsigned m[4];
+    const int c = masks(j, m);
+    int wt;
+    unsigned at = base + (unsigned)warp_excl_scan(c, &wt);
+    if (j < r1 && (j & ((1 << lhs) - 1)) == 0) lo[j >> lhs] = at;  // entries before row j
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (m[e]) dst[at++] = (m[e] << 24) | (uint32_t)(j + e);
+    base += (unsigned)wt;
+  }
+  if (Grp::tid() == 0)
+    for (int q = S > 0 ? ((S + (1 << lhs) - 1) >> lhs) : 0; q <= 2 * p.nA; ++q) lo[q] = total;
+  Grp::sync();  // sh.scan is reused by the next block scan
+}
+
 // ------------------------------------------------------------------ item A
 template <typename T, int G_T, int VEC, int LPR1>
 __device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t* tile, int rows_here,
-                                             const float (&q1)[G_T][VEC], int G, uint32_t* keys0, uint32_t* kl,
-                                             float* approx0, uint32_t* hist, int HB, int hshift) {
+                                             const float (&q1)[G_T][VEC], int G, uint32_t* keys0, size_t kst,
+                                             uint32_t* kl, float* approx0, uint32_t* hist, int HB, int hshift) {
   constexpr int E = sizeof(T);
   constexpr int RPW1 = 32 / LPR1;
   constexpr int U = G_T >= 4 ? 2 : 4;  // independent rows in flight per lane (register budget: 2 CTAs / SM)
@@ -561,7 +774,7 @@ __device__ __forceinline__ void lead_consume(const PipeParams& p, const uint8_t*
           const int rr = (ps + u) * RPW1 + r;
           if (sl == 0 && rr < rows_here) {
             const uint32_t key = order_key(acc[u]);
-            keys0[(size_t)g * p.kstride + rr] = key;
+            keys0[(size_t)g * kst + rr] = key;
             if (kl != nullptr) kl[g * p.Lc + rr] = key;
             if (approx0 != nullptr) approx0[(size_t)g * p.S_cap + rr] = acc[u];
             atomicAdd(&hist[g * HB + (key >> hshift)], 1u);
@@ -639,7 +852,7 @@ __device__ __forceinline__ void lead_consume_lpr(const PipeParams& p, const uint
 // (g8, t4) holds rows {g8, g8 + 8} x heads {2 t4, 2 t4 + 1} of each 16-row block.
 template <int RB, int G_T>
 __device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint8_t* tile, int rows_here,
-                                                 const uint32_t (&qf)[3][4][2], int G, uint32_t* keys0,
+                                                 const uint32_t (&qf)[3][4][2], int G, uint32_t* keys0, size_t kst,
                                                  uint32_t* kl, float* approx0, uint32_t* hist, int HB, int hshift) {
   constexpr int KS = RB / 32;  // k-steps of 16 bf16 columns
   const int lane = lane_id();
@@ -669,7 +882,7 @@ __device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint
       if (h < G && rr < rows_here) {
         const float sc = (S[0][i] + S[1][i]) + S[2][i];
         const uint32_t key = order_key(sc);
-        keys0[(size_t)h * p.kstride + rr] = key;
+        keys0[(size_t)h * kst + rr] = key;
         if (kl != nullptr) kl[h * p.Lc + rr] = key;
         if (approx0 != nullptr) approx0[(size_t)h * p.S_cap + rr] = sc;
         atomicAdd(&hist[h * HB + (key >> hshift)], 1u);
@@ -678,10 +891,10 @@ __device__ __forceinline__ void lead_consume_mma(const PipeParams& p, const uint
   }
 }
 
-template <typename T, int G_T, int VEC>
+template <typename T, int G_T, int VEC, bool ONCHIP = false>
 __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, int c, uint8_t* ring,
-                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, uint32_t* kloc, uint64_t* sbar,
-                       unsigned& sphase, RingPos& rp, PipeShared& sh) {
+                       uint8_t* wring, uint64_t* wbar, uint32_t* hist, uint32_t* kloc, uint32_t* kchip,
+                       uint64_t* sbar, unsigned& sphase, RingPos& rp, PipeShared& sh) {
   constexpr int E = sizeof(T);
   const int tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int nsw = p.nst, SB = p.stage_bytes;
@@ -693,6 +906,8 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
   const int row0 = c * p.La;
   const int n = max(0, min(S - row0, p.La));
   const int HB = 1 << p.hbits, hshift = 32 - p.hbits;
+  // a single-chunk unit (lists mode, the A-only launch) keeps its keys on chip and selects right here
+  const bool onchip = ONCHIP && nparts == 1;
   for (int i = tid; i < G * HB; i += kPT) hist[i] = 0u;
   __syncthreads();
   if (n > 0) {
@@ -720,7 +935,8 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
         const int col = sl * VEC + v;
         q1[g][v] = (g < G && col < p.d && sl < nch1) ? p.q_hat[(qrow0 + g) * p.D + col] : 0.f;
       }
-    uint32_t* keys_u = p.keys + (size_t)u * G * p.kstride + row0;
+    uint32_t* keys_u = onchip ? kchip : p.keys + (size_t)u * G * p.kstride + row0;
+    const size_t kst = onchip ? (size_t)p.La : (size_t)p.kstride;  // head stride of the key rows
     // spec: the chunk's keys also stay in shared memory ([G][Lc], the idle B-item entry region)
     auto kl0 = [&](int box) -> uint32_t* { return p.spec ? kloc + box * p.r1 : nullptr; };
     float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap + row0 : nullptr;
@@ -755,9 +971,9 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
           uint32_t* k0 = keys_u + i * R1;
           float* a0 = approx_u ? approx_u + i * R1 : nullptr;
           if (p.lead_swz == 64)
-            lead_consume_mma<64, G_T>(p, tile, rows_here, qf, G, k0, kl0(i), a0, hist, HB, hshift);
+            lead_consume_mma<64, G_T>(p, tile, rows_here, qf, G, k0, kst, kl0(i), a0, hist, HB, hshift);
           else
-            lead_consume_mma<128, G_T>(p, tile, rows_here, qf, G, k0, kl0(i), a0, hist, HB, hshift);
+            lead_consume_mma<128, G_T>(p, tile, rows_here, qf, G, k0, kst, kl0(i), a0, hist, HB, hshift);
           __syncwarp();
           if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
         }
@@ -801,12 +1017,12 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
       uint32_t* k0 = keys_u + i * R1;
       float* a0 = approx_u ? approx_u + i * R1 : nullptr;
       switch (LPR1) {
-        case 1: lead_consume<T, G_T, VEC, 1>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 2: lead_consume<T, G_T, VEC, 2>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 4: lead_consume<T, G_T, VEC, 4>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 8: lead_consume<T, G_T, VEC, 8>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        case 16: lead_consume<T, G_T, VEC, 16>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
-        default: lead_consume<T, G_T, VEC, 32>(p, tile, rows_here, q1, G, k0, kl0(i), a0, hist, HB, hshift); break;
+        case 1: lead_consume<T, G_T, VEC, 1>(p, tile, rows_here, q1, G, k0, kst, kl0(i), a0, hist, HB, hshift); break;
+        case 2: lead_consume<T, G_T, VEC, 2>(p, tile, rows_here, q1, G, k0, kst, kl0(i), a0, hist, HB, hshift); break;
+        case 4: lead_consume<T, G_T, VEC, 4>(p, tile, rows_here, q1, G, k0, kst, kl0(i), a0, hist, HB, hshift); break;
+        case 8: lead_consume<T, G_T, VEC, 8>(p, tile, rows_here, q1, G, k0, kst, kl0(i), a0, hist, HB, hshift); break;
+        case 16: lead_consume<T, G_T, VEC, 16>(p, tile, rows_here, q1, G, k0, kst, kl0(i), a0, hist, HB, hshift); break;
+        default: lead_consume<T, G_T, VEC, 32>(p, tile, rows_here, q1, G, k0, kst, kl0(i), a0, hist, HB, hshift); break;
       }
       __syncwarp();  // every lane is done with the slot before it is refilled
       if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
@@ -841,6 +1057,20 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
         if (m && at < (unsigned)p.ccap) cb[at] = comp_key(key, row0 + j);
       }
     }
+  }
+  if constexpr (ONCHIP) if (onchip) {
+    if (p.trace != nullptr && tid == 0) sh.t_sel = globaltimer();
+    sel_stamp(p, u, 0);
+    select_onchip<G_T>(p, u, S, kchip, p.La, hist, ring, p.nst * kPW * p.stage_bytes, sh);
+    sel_stamp(p, u, 4);
+    emit_lists<G_T>(p, u, S, kchip, p.La, sh);
+    sel_stamp(p, u, 5);
+    if (tid == 0) {  // every thread's list stores precede the release (barrier, then a gpu-scope fence)
+      __threadfence();
+      st_release(&p.ctrl[2 + 4 * (size_t)u + 2], 1u);
+    }
+    sel_stamp(p, u, 6);
+    return 3;
   }
   uint32_t* gh = p.hist + (size_t)u * G * HB;
   for (int i = tid; i < G * HB; i += kPT) {
@@ -1322,12 +1552,19 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   const int narrive = half < 0 ? nparts : 2 * nparts;     // B items of this unit
   uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
   if (tid == 0) {
-    unsigned long long spins = 0;
+    // a unit's selection is published by a CTA that is already running, so the wait always ends; the
+    // guard turns a broken invariant into an error instead of a hung GPU (p.spin_ns, 0 = no guard)
+    unsigned spins = 0;
+    long long t_start = 0;
     while (ld_acquire(&cu[2]) == 0u) {
       __nanosleep(64);
-      if (++spins > (1ull << 28)) {
-        printf("loki pipe: unit %d never became ready (block %d)\n", u, (int)blockIdx.x);
-        __trap();
+      if ((++spins & 1023u) == 0u && p.spin_ns > 0) {
+        const long long now = globaltimer();
+        if (t_start == 0) t_start = now;
+        else if (now - t_start > p.spin_ns) {
+          printf("loki pipe: unit %d never became ready (block %d)\n", u, (int)blockIdx.x);
+          __trap();
+        }
       }
     }
   }
@@ -1338,7 +1575,14 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   float* apx = reinterpret_cast<float*>(ents + p.Lc);  // [G][Lc] phase-1 partial logits, log2 domain
   // this part's selected rows, ascending, with head masks: one L2 round trip for the keys
   int n = 0;
-  if (nrows > 0) {
+  if (nrows > 0 && p.lists) {  // the A item published this unit's ordered entries and their part offsets
+    const uint32_t* lo = p.loff + (size_t)u * (2 * p.nA + 1);
+    const int h0 = half < 0 ? 2 * q : 2 * q + half;
+    const int e0 = (int)__ldcg(&lo[h0]);
+    n = (int)__ldcg(&lo[h0 + (half < 0 ? 2 : 1)]) - e0;
+    const uint32_t* src = p.sel + (size_t)u * p.kstride + e0;
+    for (int i = tid; i < n; i += kPT) ents[i] = __ldcg(&src[i]);
+  } else if (nrows > 0) {
     const uint32_t* kbase = p.keys + (size_t)u * G * p.kstride;
     unsigned long long Tc[G_T];
 #pragma unroll
@@ -1445,7 +1689,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
 
   const int ldp = D + 2;
   float* wpart = reinterpret_cast<float*>(ring);  // [kPW][G_T][D + 2]; every ring slot has been consumed
-  const int row_base = (int)(((long long)b * p.Hkv + hk) * p.unit_rows);
+  const int row_base = (int)((long long)b * p.row_sb + (long long)hk * p.row_sh);
   if constexpr (sizeof(T) == 2) {  // bf16: always the tensor-core phase 3 (host sets p.mma)
     if constexpr (D_T == 128 && G_T <= 4) {
       if (p.split_k)  // host: split-K on the tensor-core path means d == 32
@@ -1511,6 +1755,7 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
   uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + p.off_bars) + (size_t)w * nsw;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + p.off_hist);
   uint32_t* ents = reinterpret_cast<uint32_t*>(smem + p.off_ents);
+  uint32_t* kchip = reinterpret_cast<uint32_t*>(smem + p.off_kchip);  // lists mode: a unit's keys [G][La]
   uint64_t* sbar = reinterpret_cast<uint64_t*>(smem + p.off_bars) + (size_t)kPW * nsw;  // selection key stream
   unsigned sphase = 0u;
   if (lane == 0) {
@@ -1550,23 +1795,37 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
         break;
       }
       if (tid == 0) sh.next_ticket = atomicAdd(&tk[0], 1u);
-      if constexpr (MODE == 1) {
-        item_A<T, G_T, VEC>(p, &lead_map, (int)(t / (unsigned)p.nAa), (int)(t % (unsigned)p.nAa), ring, wring, wbar,
-                            hist, ents, sbar, sphase, rp, sh);
+      const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
+      int kind = 0;
+      if constexpr (MODE == 3) {
+        kind = item_A<T, G_T, VEC, true>(p, &lead_map, (int)(t / (unsigned)p.nAa), (int)(t % (unsigned)p.nAa), ring, wring,
+                                  wbar, hist, ents, kchip, sbar, sphase, rp, sh);
+      } else if constexpr (MODE == 1) {
+        kind = item_A<T, G_T, VEC>(p, &lead_map, (int)(t / (unsigned)p.nAa), (int)(t % (unsigned)p.nAa), ring, wring, wbar,
+                            hist, ents, kchip, sbar, sphase, rp, sh);
       } else {
         if ((long long)t < nfull) {
-          item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, (int)(t / (unsigned)p.nA),
-                                        (int)(t % (unsigned)p.nA), -1, ring, wring, wbar, ents, rp, sh);
+          kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, (int)(t / (unsigned)p.nA),
+                                               (int)(t % (unsigned)p.nA), -1, ring, wring, wbar, ents, rp, sh);
         } else {
           const long long tt = t - nfull;
           const int r = (int)(tt % (2 * p.nA));
-          item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map,
+          kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map,
                                         p.units - tailU + (int)(tt / (2 * p.nA)), r >> 1, r & 1, ring, wring, wbar,
                                         ents, rp, sh);
         }
       }
       fence_proxy_async();
       __syncthreads();
+      if (p.trace != nullptr && tid == 0) {  // split layers: the host gives each launch its own trace rows
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        long long* tr = p.trace + (size_t)t * 4;
+        tr[0] = t0;
+        tr[1] = globaltimer();
+        tr[2] = (long long)smid | ((long long)kind << 16) | ((long long)blockIdx.x << 32);
+        tr[3] = (kind >= 2) ? sh.t_sel : 0;
+      }
     }
     if constexpr (MODE == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
     return;
@@ -1593,7 +1852,7 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
                                       p.halves ? r >> 1 : r, p.halves ? (r & 1) : -1, ring, wring, wbar, ents,
                                       rp, sh);
     } else if (r < p.nAa) {
-      kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, sbar, sphase, rp, sh);
+      kind = item_A<T, G_T, VEC>(p, &lead_map, slot, r, ring, wring, wbar, hist, ents, kchip, sbar, sphase, rp, sh);
     } else if (slot >= p.lag && r < p.nAa + (p.halves == 2 ? 2 * p.nA : p.nA)) {
       const int rb = r - p.nAa;
       kind = item_B<T, G_T, VEC, D_T, BIG>(p, &krow_map, &vrow_map, &krow64_map, slot - p.lag,
@@ -1610,6 +1869,160 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
       tr[1] = globaltimer();
       tr[2] = (long long)smid | ((long long)kind << 16) | ((long long)blockIdx.x << 32);
       tr[3] = (kind >= 2) ? sh.t_sel : 0;
+    }
+  }
+}
+
+
+// ------------------------------------------------------------------ warp-specialised A launch
+// Split layers whose units are one A chunk (lists mode, MHA): a 16-warp CTA per
+// SM runs phase 1 and the selection as a two-stage pipeline over units.
+//   stream group (warps 0-7): draws a unit, streams its lead columns through the
+//     per-warp TMA rings, keeps the order keys and the level-0 histogram on chip
+//     in one of two buffers, hands the buffer over and starts the next unit;
+//   select group (warps 8-15): selects on the handed-over buffer (select_onchip),
+//     publishes the ordered entry lists (emit_lists) and the unit's ready flag,
+//     returns the buffer.
+// So the selection never stalls the HBM stream (the old A item streamed, then
+// selected with the SM's loads idle).  Hand-over is two mbarriers per buffer
+// (full: stream -> select, empty: select -> stream).
+using StreamGrp = WarpGroup<0, kPW, 1>;
+using SelectGrp = WarpGroup<kPW, kPW, 2>;
+
+template <typename T, int RB>
+__global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParams p,
+                                                                 const __grid_constant__ CUtensorMap lead_map) {
+  constexpr int E = sizeof(T);
+  constexpr int Q2 = RB / (2 * E);
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ PipeShared sh;
+  __shared__ int item_u[2];
+  __shared__ unsigned s_ticket;
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int lane = lane_id(), wid = warp_id();
+  const int nsw = p.nst, SB = p.stage_bytes;
+  const int HB = 1 << p.hbits, hshift = 32 - p.hbits;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bars);
+  uint64_t* full = bars + (size_t)kPW * nsw;  // [2]
+  uint64_t* empty = full + 2;                 // [2]
+  uint32_t* hist2 = reinterpret_cast<uint32_t*>(smem + p.off_hist);   // [2][HB]
+  uint32_t* kbuf2 = reinterpret_cast<uint32_t*>(smem + p.off_kchip);  // [2][La]
+  uint8_t* cand = smem + p.off_cand;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPW * nsw; ++i) mbar_init(&bars[i], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_desc(&lead_map);
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended rows
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (wid < kPW) {  // ---------------- stream group
+    const int w = wid, tid = StreamGrp::tid();
+    uint8_t* wring = smem + p.off_ring + (size_t)w * nsw * SB;
+    uint64_t* wbar = bars + (size_t)w * nsw;
+    RingPos rp(nsw);
+    for (int i = 0;; ++i) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait(&empty[b], ((i >> 1) - 1) & 1u);  // the select group is done with buffer b
+      if (tid == 0) s_ticket = atomicAdd(&p.ctrl[0], 1u);
+      StreamGrp::sync();
+      const unsigned t = s_ticket;
+      StreamGrp::sync();  // s_ticket is rewritten next round only after this
+      if ((long long)t >= p.n_tickets) {
+        if (tid == 0) {
+          item_u[b] = -1;
+          mbar_arrive(&full[b]);
+          if (atomicAdd(&p.ctrl[1], 1u) == gridDim.x - 1u) {  // last CTA out resets the counters
+            atomicExch(&p.ctrl[0], 0u);
+            atomicExch(&p.ctrl[1], 0u);
+          }
+        }
+        break;
+      }
+      const int u = (int)t;
+      const int bb = u / p.Hkv, hk = u % p.Hkv;
+      int S = p.lens[bb];
+      S = S < 0 ? 0 : (S > p.S_max ? p.S_max : S);
+      uint32_t* hist = hist2 + (size_t)b * HB;
+      uint32_t* keys = kbuf2 + (size_t)b * p.La;
+      for (int j = tid; j < HB; j += kPT) hist[j] = 0u;
+      StreamGrp::sync();
+      const int n = S < p.La ? S : p.La;
+      if (n > 0) {
+        const int R1 = p.r1;
+        const int nbox = ceil_div(n, R1);
+        const unsigned box_bytes = (unsigned)(R1 * p.dbox * E);
+        const int mine = nbox > w ? ceil_div(nbox - w, kPW) : 0;
+        auto issue = [&](int k, const RingPos& at) {
+          mbar_expect_tx(&wbar[at.slot], box_bytes);
+          tma_box4d(wring + at.slot * SB, &lead_map, 0, (w + k * kPW) * R1, hk, bb, &wbar[at.slot]);
+        };
+        if (lane == 0) {
+          RingPos q = rp;
+          for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
+        }
+        const size_t qrow0 = (size_t)bb * p.Hq + (size_t)hk;
+        unsigned long long q2[Q2];
+#pragma unroll
+        for (int j = 0; j < Q2; ++j) {
+          const int c0 = 2 * j, c1 = 2 * j + 1;
+          const float a = c0 < p.d ? p.q_hat[qrow0 * p.D + c0] : 0.f;
+          const float bq = c1 < p.d ? p.q_hat[qrow0 * p.D + c1] : 0.f;
+          q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
+        }
+        float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap : nullptr;
+        for (int k = 0; k < mine; ++k, rp.advance(1)) {
+          mbar_wait(&wbar[rp.slot], rp.phase);
+          const int box = w + k * kPW;
+          const int rows_here = min(R1, n - box * R1);
+          lead_consume_lpr<T, RB>(p, wring + rp.slot * SB, rows_here, q2, keys + box * R1, nullptr,
+                                  approx_u ? approx_u + box * R1 : nullptr, hist, hshift);
+          __syncwarp();
+          if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+        }
+      }
+      StreamGrp::sync();  // every key and histogram count of this unit is in shared memory
+      if (tid == 0) {
+        item_u[b] = u;
+        mbar_arrive(&full[b]);  // release: the select group acquires through the barrier phase
+      }
+    }
+  } else {  // ---------------- select group
+    const int tid = SelectGrp::tid();
+    for (int i = 0;; ++i) {
+      const int b = i & 1;
+      mbar_wait(&full[b], (i >> 1) & 1u);
+      const int u = item_u[b];
+      if (u < 0) break;
+      int S = p.lens[u / p.Hkv];
+      S = S < 0 ? 0 : (S > p.S_max ? p.S_max : S);
+      const uint32_t* keys = kbuf2 + (size_t)b * p.La;
+      const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
+      sel_stamp<SelectGrp>(p, u, 0);
+      select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
+      sel_stamp<SelectGrp>(p, u, 4);
+      emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
+      sel_stamp<SelectGrp>(p, u, 5);
+      if (tid == 0) {
+        __threadfence();  // the group's list stores (ordered by the barrier) before the release
+        st_release(&p.ctrl[2 + 4 * (size_t)u + 2], 1u);
+        mbar_arrive(&empty[b]);
+        if (p.trace != nullptr) {  // one row per unit: {select start, end, smid | kind 3, select start}
+          unsigned smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          long long* tr = p.trace + (size_t)u * 4;
+          tr[0] = t0;
+          tr[1] = globaltimer();
+          tr[2] = (long long)smid | (3LL << 16) | ((long long)blockIdx.x << 32);
+          tr[3] = t0;
+        }
+      }
+      sel_stamp<SelectGrp>(p, u, 6);
     }
   }
 }
@@ -1658,6 +2071,10 @@ cudaError_t pipe_launch_dt(const PipeParams& p, int G_T, int grid, size_t smem, 
                            bool big, int mode) {
   constexpr int V = sizeof(T) == 2 ? 8 : 4;
   if constexpr (sizeof(T) == 2) {  // split layers: bf16 caches
+    if (mode == 3) {  // A-only launch with on-chip selection (lists mode: MHA, single-chunk units)
+      if (G_T == 1 && !big) return launch_pipe_t<T, 1, V, DT, false, 3>(p, grid, smem, maps, st);
+      return cudaErrorInvalidValue;
+    }
     if (mode != 0) {
       switch (G_T) {
         case 1:
@@ -1700,6 +2117,7 @@ template <typename T, int DT>
 int pipe_occ_dt(int G_T, size_t smem, bool big, int mode) {
   constexpr int V = sizeof(T) == 2 ? 8 : 4;
   if constexpr (sizeof(T) == 2) {
+    if (mode == 3) return (G_T == 1 && !big) ? occupancy_t<T, 1, V, DT, false, 3>(smem) : 0;
     if (mode != 0) {
       switch (G_T) {
         case 1:

@@ -11,7 +11,7 @@ for p in $parts; do
     ref) timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; cat gpurun_out/bench_ref.json | head -c 1500; tail -3 gpurun_out/bench_ref.err ;;
     sanitize)
       for tool in memcheck synccheck racecheck; do
-        timeout 600 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
+        LOKI_TUNING=1 LOKI_SPIN_S=100000 timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
         echo "sanitizer $tool rc=$?"; tail -4 gpurun_out/sanitize_$tool.log
       done ;;
   esac

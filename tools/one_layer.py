@@ -102,7 +102,7 @@ if os.environ.get("LOKI_TRACE") and call.plan()["ctas_per_unit"] <= 0:
         st8 = buf.view(-1).cpu().numpy()[1 << 21:(1 << 21) + a.B * a.Hkv * 8].reshape(-1, 8)
         ok = st8[:, 0] != 0
         st8 = st8[ok]
-        names = ["hist+find_bin", "compaction", "narrow", "rank", "offsets/misc", "fence+release"]
+        names = ["find_bin", "compaction", "narrow+rank", "other heads", "emit/offsets", "fence+release"]
         for i, nm in enumerate(names):
             dd = (st8[:, i + 1] - st8[:, i]) / 1e3
             print(f"    sel {nm:14s} median {np.median(dd):6.2f} us  max {dd.max():6.2f}")
