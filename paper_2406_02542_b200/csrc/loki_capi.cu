@@ -247,6 +247,7 @@ struct PipePlan {
   bool big = false;
   bool split = false;  // A-only launch + B-only launch (MHA bf16)
   bool ws_select = false;  // the A launch is the warp-specialised pipe_select_kernel (layout in sel_layout)
+  bool ws_onchip = false;  // ... with the keys on chip (lists mode)
   loki::PipeParams sel_layout{};
   int grid = 0, grid1 = 0, grid2 = 0;
   size_t smem1 = 0;
@@ -376,23 +377,38 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // histogram merge, no L2 key re-stream; B items copy their slice).  Needs the unit's keys on chip next
   // to the ring: the A-only launch of a split layer carries them in place of the B-entry region
   p.lists = 0;
-  const size_t kchip = (size_t)G_T * p.La * 4;
-  if (pl->split && G_T == 1 && !pl->big && env_int("LOKI_LISTS", 1) != 0 && p.nAa == 1 && !p.spec && !p.split_k &&
-      a->idx_out == nullptr && a->weights_out == nullptr && ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0 && p.Lc / 2 >= 4) {
-    // preferred: the warp-specialised A launch (stream group + select group, one 16-warp CTA per SM)
+  if (pl->split && G_T == 1 && !p.spec && !p.split_k && a->idx_out == nullptr &&
+      a->weights_out == nullptr && (p.lead_swz == 64 || p.lead_swz == 128) && env_int("LOKI_SELECT_WS", 1) != 0 &&
+      units >= sm_count()) {
+    // The warp-specialised A launch (one 16-warp CTA per SM, one whole unit per item): a stream group
+    // streams unit i's lead columns while a select group selects unit i - 1, so the selection never
+    // idles the loads.  Units of <= 8192 rows keep their keys on chip and publish ordered entry lists
+    // (lists mode); longer ones keep the keys in the workspace and publish the threshold.
     loki::PipeParams ps = p;
-    const size_t sw = loki::pipe_select_layout(&ps);
-    const int ow = (p.lead_swz == 64 || p.lead_swz == 128) && env_int("LOKI_SELECT_WS", 1) != 0
-                       ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, sw) : 0;
-    const size_t s1 = (size_t)p.off_ents + kchip + 1024;
-    const int o1 = ow >= 1 ? 0 : loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, s1, pl->big, 3);
-    if (sw <= kSmemMax && ow >= 1) {
-      p.lists = 1;
+    ps.La = loki::ceil_div(a->S_max, p.r1) * p.r1;
+    ps.nAa = 1;
+    const bool onchip = ps.La <= env_int("LOKI_ONCHIP_ROWS", 8192) && ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0;
+    const size_t sw = loki::pipe_select_layout(&ps, onchip);
+    const int ow = sw <= kSmemMax ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, onchip, sw) : 0;
+    if (ow >= 1) {
+      p.La = ps.La;
+      p.nAa = 1;
+      p.lists = onchip ? 1 : 0;
       pl->ws_select = true;
+      pl->ws_onchip = onchip;
       pl->sel_layout = ps;
       pl->smem1 = sw;
       pl->grid1 = sm_count() * ow;
-    } else if (s1 <= kSmemMax && o1 >= 1) {  // MODE 3: the A-only launch carries the keys in place of the B entries
+    }
+  }
+  const size_t kchip = (size_t)G_T * p.La * 4;
+  if (!pl->ws_select && pl->split && G_T == 1 && !pl->big && env_int("LOKI_LISTS", 0) != 0 && p.nAa == 1 &&
+      !p.spec && !p.split_k && a->idx_out == nullptr && a->weights_out == nullptr &&
+      ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0 && p.Lc / 2 >= 4) {
+    // MODE 3 (opt-in): the A-only launch selects on chip, the keys in place of the B-entry region
+    const size_t s1 = (size_t)p.off_ents + kchip + 1024;
+    const int o1 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, s1, pl->big, 3);
+    if (s1 <= kSmemMax && o1 >= 1) {
       p.lists = 1;
       p.off_kchip = p.off_ents;
       pl->smem1 = s1;
@@ -513,7 +529,8 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
       pa.off_kchip = pl.sel_layout.off_kchip;
       pa.off_cand = pl.sel_layout.off_cand;
       pa.cand_bytes = pl.sel_layout.cand_bytes;
-      e = loki::launch_pipe_select(pa, g.dtype, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream));
+      e = loki::launch_pipe_select(pa, g.dtype, pl.ws_onchip, pl.grid1, pl.smem1, maps,
+                                   static_cast<cudaStream_t>(stream));
     } else {
       e = loki::launch_pipe(pa, g.dtype, pl.G_T, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big,
                             p.lists ? 3 : 1);

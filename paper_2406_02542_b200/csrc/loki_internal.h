@@ -180,12 +180,13 @@ bool encode_pipe_tma(const void* K, const void* V, const loki_kv_geom& g, int db
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
                         cudaStream_t st, bool big, int mode = 0);
 int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode = 0);
-// warp-specialised A launch of lists-mode split layers (MHA bf16, lead rows of 64 / 128 B): sets the
-// layout offsets in *p (ring, bars, double-buffered histograms and keys, candidates) and returns its bytes
-size_t pipe_select_layout(PipeParams* p);
-int pipe_select_ctas_per_sm(int dtype, int lead_rb, size_t smem);
-cudaError_t launch_pipe_select(const PipeParams& p, int dtype, int grid, size_t smem, const TmaDesc* maps,
-                               cudaStream_t st);
+// warp-specialised A launch of split MHA bf16 layers (lead rows of 64 / 128 B), one unit per item: sets the
+// layout offsets in *p (ring, bars, double-buffered histograms, on-chip keys or the key stream's buffers,
+// candidates) and returns its bytes.  onchip: keys on chip + lists mode; else keys in the workspace
+size_t pipe_select_layout(PipeParams* p, bool onchip);
+int pipe_select_ctas_per_sm(int dtype, int lead_rb, bool onchip, size_t smem);
+cudaError_t launch_pipe_select(const PipeParams& p, int dtype, bool onchip, int grid, size_t smem,
+                               const TmaDesc* maps, cudaStream_t st);
 int pipe_warps();
 // 128-row blocks per warp in a B part (Lc = blocks * 128 * warps), shared by kernel and host
 __host__ __device__ constexpr int pipe_blocks_per_warp(int G_T, bool big) {

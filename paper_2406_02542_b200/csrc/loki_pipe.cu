@@ -56,43 +56,45 @@ int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode)
   return 0;
 }
 
-size_t pipe_select_layout(PipeParams* p) {
+size_t pipe_select_layout(PipeParams* p, bool onchip) {
   size_t off = 0;
   p->off_ring = 0;
   off += (size_t)kPW * p->nst * p->stage_bytes;
   p->off_bars = (int)off;
-  off = align_up(off + (size_t)(kPW * p->nst + 4) * 8, 16);
+  off = align_up(off + (size_t)(kPW * p->nst + 6) * 8, 16);
   p->off_hist = (int)off;
   off = align_up(off + 2 * (size_t)(1u << p->hbits) * 4, 128);
-  p->off_kchip = (int)off;
-  off = align_up(off + 2 * (size_t)p->La * 4, 128);
+  p->off_kchip = (int)off;  // on-chip keys [2][La], or the key stream's two chunk buffers
+  off = align_up(off + 2 * (size_t)(onchip ? p->La : kCK) * 4, 128);
   p->off_cand = (int)off;
-  p->cand_bytes = 16 * 1024;  // 1024 boundary-bin candidates, two buffers; more -> histogram narrowing
+  p->cand_bytes = (onchip ? 16 : 32) * 1024;  // boundary-bin candidates, two buffers; more -> histogram levels
   off += (size_t)p->cand_bytes;
   return off + 1024;  // slack for aligning the dynamic shared memory base to 1024 B
 }
 
-template <typename T, int RB>
+template <int RB, bool ONCHIP>
 KernelAttrs& select_attrs() {
   static KernelAttrs a;
   return a;
 }
 
-int pipe_select_ctas_per_sm(int dtype, int lead_rb, size_t smem) {
+template <int RB, bool ONCHIP>
+static int select_occ(size_t smem) {
+  return select_attrs<RB, ONCHIP>().occupancy(
+      reinterpret_cast<const void*>(pipe_select_kernel<__nv_bfloat16, RB, ONCHIP>), 2 * kPT, smem);
+}
+
+int pipe_select_ctas_per_sm(int dtype, int lead_rb, bool onchip, size_t smem) {
   if (dtype != LOKI_DTYPE_BF16) return 0;
-  if (lead_rb == 64)
-    return select_attrs<__nv_bfloat16, 64>().occupancy(
-        reinterpret_cast<const void*>(pipe_select_kernel<__nv_bfloat16, 64>), 2 * kPT, smem);
-  if (lead_rb == 128)
-    return select_attrs<__nv_bfloat16, 128>().occupancy(
-        reinterpret_cast<const void*>(pipe_select_kernel<__nv_bfloat16, 128>), 2 * kPT, smem);
+  if (lead_rb == 64) return onchip ? select_occ<64, true>(smem) : select_occ<64, false>(smem);
+  if (lead_rb == 128) return onchip ? select_occ<128, true>(smem) : select_occ<128, false>(smem);
   return 0;
 }
 
-template <int RB>
+template <int RB, bool ONCHIP>
 static cudaError_t launch_select_t(const PipeParams& p, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st) {
-  auto kern = pipe_select_kernel<__nv_bfloat16, RB>;
-  cudaError_t e = select_attrs<__nv_bfloat16, RB>().ensure(reinterpret_cast<const void*>(kern), smem);
+  auto kern = pipe_select_kernel<__nv_bfloat16, RB, ONCHIP>;
+  cudaError_t e = select_attrs<RB, ONCHIP>().ensure(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -108,11 +110,14 @@ static cudaError_t launch_select_t(const PipeParams& p, int grid, size_t smem, c
   return cudaLaunchKernelEx(&cfg, kern, p, m[0]);
 }
 
-cudaError_t launch_pipe_select(const PipeParams& p, int dtype, int grid, size_t smem, const TmaDesc* maps,
-                               cudaStream_t st) {
+cudaError_t launch_pipe_select(const PipeParams& p, int dtype, bool onchip, int grid, size_t smem,
+                               const TmaDesc* maps, cudaStream_t st) {
   if (dtype != LOKI_DTYPE_BF16) return cudaErrorInvalidValue;
-  if (p.lead_swz == 64) return launch_select_t<64>(p, grid, smem, maps, st);
-  if (p.lead_swz == 128) return launch_select_t<128>(p, grid, smem, maps, st);
+  if (p.lead_swz == 64)
+    return onchip ? launch_select_t<64, true>(p, grid, smem, maps, st) : launch_select_t<64, false>(p, grid, smem, maps, st);
+  if (p.lead_swz == 128)
+    return onchip ? launch_select_t<128, true>(p, grid, smem, maps, st)
+                  : launch_select_t<128, false>(p, grid, smem, maps, st);
   return cudaErrorInvalidValue;
 }
 

@@ -1874,6 +1874,183 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
 }
 
 
+// Keys of one unit streamed from L2 through two shared buffers of kCK keys
+// (cp.async.bulk, the next chunk in flight while this one is scanned), run by a
+// thread group.  `sbar` are the group's two mbarriers, `sphase` their parities.
+template <typename Grp>
+struct KeyStreamG {
+  const uint32_t* src;
+  int S, kstride;
+  uint32_t* buf;  // [2][kCK]
+  uint64_t* sbar;
+  unsigned* sphase;
+  int nchunk;
+  __device__ void issue(int c) const {
+    if (Grp::tid() == 0 && c < nchunk) {
+      const int base = c * kCK;
+      const int rows = min(kCK, kstride - base);
+      const unsigned bytes = (unsigned)(((rows * 4) + 15) & ~15);
+      uint64_t* bar = &sbar[c & 1];
+      mbar_expect_tx(bar, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(buf + (c & 1) * kCK)),
+          "l"(src + base), "r"(bytes), "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
+  __device__ void start() const {
+    if (Grp::tid() == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // keys came from generic stores
+    issue(0);
+    issue(1);
+  }
+  template <typename F>
+  __device__ void run(F&& f) const {
+    for (int c = 0; c < nchunk; ++c) {
+      const int bi = c & 1;
+      mbar_wait(&sbar[bi], (*sphase >> bi) & 1u);
+      *sphase ^= 1u << bi;
+      f(c * kCK, buf + bi * kCK, min(kCK, S - c * kCK));
+      Grp::sync();  // the whole group is done with buffer bi before it is refilled
+      issue(c + 2);
+    }
+  }
+};
+
+// Selection of a whole unit (one head) whose level-0 histogram is on chip but
+// whose keys are in the L2-resident workspace (too many rows to keep on chip):
+// the select group of the warp-specialised A launch, for long MHA sequences.
+// Same composite-key rule as select_unit / select_onchip; publishes tcs[u].
+template <typename Grp>
+__device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, uint32_t* kbuf, uint64_t* sbar,
+                              unsigned& sphase, uint8_t* scratch, int scratch_bytes, PipeShared& sh) {
+  const int tid = Grp::tid(), lane = lane_id();
+  const int hb = p.hbits, HB = 1 << hb;
+  const int kb = k_of(p, S);
+  const int cap = scratch_bytes / 16;
+  unsigned long long* candA = reinterpret_cast<unsigned long long*>(scratch);
+  unsigned long long* candB = candA + cap;
+  const uint32_t* keys = p.keys + (size_t)u * p.kstride;
+  const KeyStreamG<Grp> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S > 0 ? S : 1, kCK)};
+  unsigned long long Tc;
+  if (kb <= 0 || kb >= S) {
+    Tc = kb <= 0 ? ~0ull : 0ull;
+  } else {
+    ks.start();  // the compaction pass below almost always runs
+    bool started = true;
+    find_bin<Grp>(h, HB, (unsigned)kb, sh);
+    sel_stamp<Grp>(p, u, 1);
+    unsigned long long P = (unsigned long long)sh.fb_bin;
+    int nb = hb;
+    unsigned need = (unsigned)kb - sh.fb_above, cnt = sh.fb_cnt;
+    int ncand = 0;
+    bool listed = false;
+    for (;;) {
+      if (cnt == need) break;
+      if (!started) ks.start();
+      started = false;
+      const int sh64 = 64 - nb;
+      if (cnt <= (unsigned)cap) {  // compact the rows matching P
+        if (tid == 0) sh.ncand = 0;
+        Grp::sync();
+        ks.run([&](int j0, const uint32_t* kc, int nrow) {
+          for (int i0 = 0; i0 < nrow; i0 += 4 * Grp::kThreads) {
+            const int il = i0 + 4 * tid;
+            uint4 kk = make_uint4(0u, 0u, 0u, 0u);
+            if (il < nrow) kk = *reinterpret_cast<const uint4*>(kc + il);
+            unsigned hit = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              hit |= (il + e < nrow && (comp_key(u4_at(kk, e), j0 + il + e) >> sh64) == P ? 1u : 0u) << e;
+            if (__any_sync(0xffffffffu, hit != 0u)) {
+              int tot;
+              const int ex = warp_excl_scan(__popc(hit), &tot);
+              int at = 0;
+              if (lane == 0) at = atomicAdd(&sh.ncand, tot);
+              at = __shfl_sync(0xffffffffu, at, 0) + ex;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if ((hit >> e) & 1u) candA[at++] = comp_key(u4_at(kk, e), j0 + il + e);
+            }
+          }
+        });
+        ncand = sh.ncand;
+        listed = true;
+        break;
+      }
+      // one more histogram level over the rows matching P
+      const int bits = min(hb, 64 - nb);
+      for (int i = tid; i < (1 << bits); i += Grp::kThreads) h[i] = 0u;
+      Grp::sync();
+      ks.run([&](int j0, const uint32_t* kc, int nrow) {
+        for (int i = tid; i < nrow; i += Grp::kThreads) {
+          const unsigned long long c = comp_key(kc[i], j0 + i);
+          if ((c >> sh64) == P) atomicAdd(&h[(c >> (sh64 - bits)) & ((1ull << bits) - 1)], 1u);
+        }
+      });
+      find_bin<Grp>(h, 1 << bits, need, sh);
+      P = (P << bits) | (unsigned long long)sh.fb_bin;
+      nb += bits;
+      need -= sh.fb_above;
+      cnt = sh.fb_cnt;
+    }
+    if (started) {  // the prefetched chunks were never consumed: drain them before the buffers are reused
+      for (int c = 0; c < 2 && c < ks.nchunk; ++c) {
+        mbar_wait(&sbar[c], (sphase >> c) & 1u);
+        sphase ^= 1u << c;
+      }
+      Grp::sync();
+    }
+    sel_stamp<Grp>(p, u, 2);
+    Tc = nb >= 64 ? P : (P << (64 - nb));
+    if (listed && cnt != need) {
+      const unsigned long long* src = candA;
+      unsigned long long* dst = candB;
+      while (ncand > 32) {
+        const int bits = min(8, 64 - nb);
+        for (int i = tid; i < (1 << bits); i += Grp::kThreads) h[i] = 0u;
+        Grp::sync();
+        for (int i = tid; i < ncand; i += Grp::kThreads)
+          atomicAdd(&h[(src[i] >> (64 - nb - bits)) & ((1ull << bits) - 1)], 1u);
+        Grp::sync();
+        find_bin<Grp>(h, 1 << bits, need, sh);
+        P = (P << bits) | (unsigned long long)sh.fb_bin;
+        nb += bits;
+        need -= sh.fb_above;
+        cnt = sh.fb_cnt;
+        if (cnt == need) break;
+        if (tid == 0) sh.ncand = 0;
+        Grp::sync();
+        for (int i0 = 0; i0 < ncand; i0 += Grp::kThreads) {
+          const int i = i0 + tid;
+          const unsigned long long c = i < ncand ? src[i] : 0ull;
+          append_if(i < ncand && (c >> (64 - nb)) == P, c, dst, &sh.ncand);
+        }
+        Grp::sync();
+        ncand = sh.ncand;
+        unsigned long long* was = const_cast<unsigned long long*>(src);
+        src = dst;
+        dst = was;
+      }
+      if (cnt == need) {
+        Tc = nb >= 64 ? P : (P << (64 - nb));
+      } else {  // <= 32 candidates, one per lane of the group's first warp: the need-th largest by rank
+        if (tid < 32) {
+          const unsigned long long c = tid < ncand ? src[tid] : 0ull;
+          unsigned rank = 0;
+          for (int i = 0; i < ncand; ++i) rank += __shfl_sync(0xffffffffu, c, i) > c;
+          if (tid < ncand && rank == need - 1) sh.tsel = c;
+        }
+        Grp::sync();
+        Tc = sh.tsel;
+      }
+    }
+    sel_stamp<Grp>(p, u, 3);
+  }
+  if (tid == 0) p.tcs[u] = Tc;
+  Grp::sync();
+}
+
 // ------------------------------------------------------------------ warp-specialised A launch
 // Split layers whose units are one A chunk (lists mode, MHA): a 16-warp CTA per
 // SM runs phase 1 and the selection as a two-stage pipeline over units.
@@ -1889,7 +2066,11 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
 using StreamGrp = WarpGroup<0, kPW, 1>;
 using SelectGrp = WarpGroup<kPW, kPW, 2>;
 
-template <typename T, int RB>
+// ONCHIP: the unit's keys stay in shared memory (double-buffered [2][La]) and the
+// select group also emits the ordered entry lists (lists mode); else (long
+// sequences) the stream group writes the keys to the L2-resident workspace, the
+// select group streams them back (select_global) and publishes the threshold.
+template <typename T, int RB, bool ONCHIP>
 __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParams p,
                                                                  const __grid_constant__ CUtensorMap lead_map) {
   constexpr int E = sizeof(T);
@@ -1905,14 +2086,16 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bars);
   uint64_t* full = bars + (size_t)kPW * nsw;  // [2]
   uint64_t* empty = full + 2;                 // [2]
+  uint64_t* sbar = empty + 2;                 // [2] the select group's key stream (!ONCHIP)
   uint32_t* hist2 = reinterpret_cast<uint32_t*>(smem + p.off_hist);   // [2][HB]
-  uint32_t* kbuf2 = reinterpret_cast<uint32_t*>(smem + p.off_kchip);  // [2][La]
+  uint32_t* kbuf2 = reinterpret_cast<uint32_t*>(smem + p.off_kchip);  // ONCHIP: [2][La]; else [2][kCK]
   uint8_t* cand = smem + p.off_cand;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kPW * nsw; ++i) mbar_init(&bars[i], 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], 1);
+      mbar_init(&sbar[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_desc(&lead_map);
@@ -1949,7 +2132,7 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       int S = p.lens[bb];
       S = S < 0 ? 0 : (S > p.S_max ? p.S_max : S);
       uint32_t* hist = hist2 + (size_t)b * HB;
-      uint32_t* keys = kbuf2 + (size_t)b * p.La;
+      uint32_t* keys = ONCHIP ? kbuf2 + (size_t)b * p.La : p.keys + (size_t)u * p.kstride;
       for (int j = tid; j < HB; j += kPT) hist[j] = 0u;
       StreamGrp::sync();
       const int n = S < p.La ? S : p.La;
@@ -1994,6 +2177,7 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
     }
   } else {  // ---------------- select group
     const int tid = SelectGrp::tid();
+    unsigned sphase = 0u;
     for (int i = 0;; ++i) {
       const int b = i & 1;
       mbar_wait(&full[b], (i >> 1) & 1u);
@@ -2004,9 +2188,14 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       const uint32_t* keys = kbuf2 + (size_t)b * p.La;
       const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
       sel_stamp<SelectGrp>(p, u, 0);
-      select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
-      sel_stamp<SelectGrp>(p, u, 4);
-      emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
+      if constexpr (ONCHIP) {
+        select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
+        sel_stamp<SelectGrp>(p, u, 4);
+        emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
+      } else {
+        select_global<SelectGrp>(p, u, S, hist2 + (size_t)b * HB, kbuf2, sbar, sphase, cand, p.cand_bytes, sh);
+        sel_stamp<SelectGrp>(p, u, 4);
+      }
       sel_stamp<SelectGrp>(p, u, 5);
       if (tid == 0) {
         __threadfence();  // the group's list stores (ordered by the barrier) before the release
