@@ -110,3 +110,49 @@ def test_sharded_decode_bit_identical_on_gpu(monkeypatch, halves, B, Hq, Hkv):
             assert torch.allclose(y_sh, y_full, rtol=1e-5, atol=1e-6), world
         else:
             assert torch.equal(y_sh, y_full), world
+
+
+def _gpu_worker(rank, world, port, backend, result_path):
+    """One rank of a head-sharded decode: this rank's KV-head slice through the CUDA kernel (libloki_b200),
+    then the layer's one exchange step (sharding.gather_heads).  NCCL ranks own one GPU each; gloo ranks
+    share cuda:0 and exchange host copies (NCCL refuses two ranks on one device)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import paper_2406_02542_b200 as L
+
+    dev = torch.device("cuda", rank if backend == "nccl" else 0)
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    B, Hq, Hkv, D, S = 4, 16, 8, 128, 8192
+    g = torch.Generator(device=dev).manual_seed(17)  # every rank draws the full problem, keeps its slice
+    K = torch.randn(B, Hkv, S, D, device=dev, generator=g).to(torch.bfloat16)
+    V = torch.randn(B, Hkv, S, D, device=dev, generator=g).to(torch.bfloat16)
+    q = torch.randn(B, Hq, D, device=dev, generator=g)
+    sh = sharding.head_shard(Hq, Hkv, world, rank)
+    y = L.loki_decode(sharding.shard_heads(q, sh, kv=False).contiguous(), sharding.shard_heads(K, sh, kv=True),
+                      sharding.shard_heads(V, sh, kv=True), None, k_f=0.25, d=32)
+    full = sharding.gather_heads(y if backend == "nccl" else y.cpu(), world)
+    if rank == 0:
+        y_ref = L.loki_decode(q, K, V, None, k_f=0.25, d=32)
+        torch.cuda.synchronize()
+        np.save(result_path, np.stack([full.cpu().numpy(), y_ref.cpu().numpy()]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_two_process_kernel_shard_and_gather_bit_identical(tmp_path, backend):
+    """Two processes, each running its KV-head shard through the CUDA kernel, then the all-gather: the
+    assembled [B, Hq, D] equals one unsharded launch bit for bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip("NCCL needs one GPU per rank (fewer than 2 visible)")
+    out = str(tmp_path / "y.npy")
+    mp.start_processes(_gpu_worker, args=(2, _free_port(), backend, out), nprocs=2, join=True,
+                       start_method="spawn")
+    got, ref = np.load(out)
+    np.testing.assert_array_equal(got, ref)

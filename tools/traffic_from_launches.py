@@ -17,7 +17,7 @@ def main():
     rows = [ln for ln in open(path) if ln.startswith('"')]
     per = defaultdict(lambda: defaultdict(dict))  # kernel -> launch id -> metric -> value
     for r in csv.DictReader(rows):
-        if "pipe_decode" not in r["Kernel Name"]:
+        if "pipe_" not in r["Kernel Name"]:
             continue
         per[r["Kernel Name"]][r["ID"]][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
     res = {"kernels": {}}
