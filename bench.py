@@ -691,6 +691,45 @@ def attention_block(wl, decs, reps, world, with_dense=True):
     return blk
 
 
+def gather_compare(wl, dec, reps):
+    """R14 / criterion 7 (reference bench.py:275-321, kernels.py:297-308) at layer scale: sparse exact
+    attention over a given selection, fused (the library's gather kernel: rows read in place, scores,
+    softmax and P.V in one launch, SELECT_INDICES) vs copy-then-dense (torch materialises K[idx] and
+    V[idx], then dense SDPA on the copies).  Same selection (layer 0's), same bf16 caches."""
+    import torch
+    import torch.nn.functional as F
+
+    import paper_2406_02542_b200 as L
+    from paper_2406_02542_b200 import _core, _lib
+
+    _, diag = L.loki_decode(dec.q_hat, wl.K[0], wl.V[0], wl.lens, d=wl.d, k=wl.k, diagnostics=True)
+    idx32 = diag.indices.to(torch.int32).contiguous()
+    out = torch.empty(wl.B, wl.Hq_l, wl.D, device=wl.dev)
+    call = _core.DecodeCall(dec.q_hat, wl.K[0], wl.V[0], wl.lens, wl.S, wl.d, k_fixed=wl.k,
+                            select_mode=_lib.SELECT_INDICES, ext_idx=idx32, idx_stride=wl.k, out=out,
+                            Hq=wl.Hq_l)
+    idx64 = diag.indices.view(wl.B, wl.Hkv_l, wl.G * wl.k)
+    bi = torch.arange(wl.B, device=wl.dev)[:, None, None]
+    hi = torch.arange(wl.Hkv_l, device=wl.dev)[None, :, None]
+    qb = dec.q_hat.to(torch.bfloat16).view(wl.B, wl.Hkv_l, wl.G, wl.D)
+
+    def copy_then_dense():
+        Kg = wl.K[0][bi, hi, idx64].view(wl.B, wl.Hkv_l, wl.G, wl.k, wl.D)
+        Vg = wl.V[0][bi, hi, idx64].view(wl.B, wl.Hkv_l, wl.G, wl.k, wl.D)
+        return F.scaled_dot_product_attention(qb.unsqueeze(3), Kg, Vg)
+    call.run()
+    y_copy = copy_then_dense().view(wl.B, wl.Hq_l, wl.D).float()
+    torch.cuda.synchronize()
+    err = float((y_copy - out).abs().max() / out.abs().max())
+    fused = time_region(lambda: call.run(), reps, 1) * 1000.0 / reps
+    copied = time_region(copy_then_dense, reps, 1) * 1000.0 / reps
+    return {"fused_us": round(fused, 3), "copy_then_dense_us": round(copied, 3),
+            "copy_over_fused": round(copied / fused, 3), "criterion7_met": copied / fused >= 1.2,
+            "max_rel_diff": float(f"{err:.3e}"),
+            "what": "layer 0, all units: sparse exact attention on the Loki selection; fused gather kernel "
+                    "(SELECT_INDICES) vs torch K[idx] / V[idx] copies + SDPA"}
+
+
 def tgt_block(args, world, rank):
     """North-star shape (TGT: MHA 32 heads, B = 16, S = 32K, k_f = d_f = 0.25) measured in the default run:
     Loki attention, its roofline fraction and the speed-up over the fastest dense decode."""
@@ -767,6 +806,9 @@ def main():
     reps = max(10, args.steps // 2)
     attn = attention_block(wl, decs, reps, world, with_dense=not args.no_extras)
     fused_us = attn["loki_attention_us_per_layer"]
+    gcmp = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        gcmp = gather_compare(wl, decs[0], reps)
     append_us = max(0.0, us_layer - fused_us)
     peak, peak_src = peak_gbs()
     traffic = None
@@ -865,6 +907,7 @@ def main():
                          "algorithmic_bytes_per_launch": attn["algorithmic_bytes_per_layer"], "peak_source": peak_src,
                          "rows_gathered_per_unit": attn["rows_gathered_per_unit"]},
             "parity": parity,
+            "gather_compare": gcmp,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "tgt": tgt,

@@ -218,6 +218,65 @@ def loki_decode_batched(q_hat, K_hat, V, lens, d: int, k_f: float = None, k=None
     return y, diags
 
 
+def loki_rank_and_attend_shared(q_block, K_hat, V, d: int, k: int):
+    """Group-shared selection (opt-in GQA mode, SURVEY 7 hard part 3), composed from
+    the reference's primitives: sliced_score_kernel on the [G, D] query block
+    (kernels.py:223-241), summed over the group, ONE topk_indices (linalg.py:95-118),
+    then per query head the exact path of attention.py:180-184.
+
+    Returns (y fp32 [G, D], indices int64 [k], group scores fp32 [S], weights fp32 [G, k]).
+    """
+    Q = np.asarray(q_block, dtype=F32).reshape(-1, np.shape(K_hat)[1])
+    K = np.asarray(K_hat, dtype=F32)
+    Vm = np.asarray(V, dtype=F32)
+    S, D = K.shape
+    assert 1 <= d <= D and 1 <= k <= S
+    group = sliced_scores(Q, K, d).reshape(Q.shape[0], S).sum(axis=0, dtype=F32)
+    idx = topk_indices(group, k)
+    ys, ws = [], []
+    for g in range(Q.shape[0]):
+        y, w = attend_on(Q[g], K, Vm, idx)
+        ys.append(y)
+        ws.append(w)
+    return np.stack(ys).astype(F32), idx, group, np.stack(ws)
+
+
+def loki_decode_batched_shared(q_hat, K_hat, V, lens, d: int, k_f: float = None, k=None):
+    """Batched restatement of the group-shared mode: one selection per (b, KV head) on
+    the group's summed leading-d scores, every query head of the group attends over it.
+    Returns y [B, Hq, D] and per (b, kv head) (idx, group scores, weights [G, k])."""
+    q_hat = np.asarray(q_hat, dtype=F32)
+    B, Hq, D = q_hat.shape
+    Hkv = K_hat.shape[1]
+    G = Hq // Hkv
+    y = np.zeros((B, Hq, D), dtype=F32)
+    diags = []
+    for b in range(B):
+        S = int(lens[b])
+        kb = resolve_fraction(k_f, S) if k is None else (int(k[b]) if np.ndim(k) else int(k))
+        row = []
+        for g in range(Hkv):
+            yy, idx, grp, w = loki_rank_and_attend_shared(q_hat[b, g * G:(g + 1) * G], K_hat[b, g, :S],
+                                                          V[b, g, :S], d, kb)
+            y[b, g * G:(g + 1) * G] = yy
+            row.append((idx, grp, w))
+        diags.append(row)
+    return y, diags
+
+
+def pca_attn(q, K_hat_d, V, P_d):
+    """Attend to every token on the leading-d coordinates only, logits scaled by
+    sqrt(D) of the full head -- attention.py:209-232."""
+    q = np.asarray(q, dtype=F32).reshape(-1)
+    K = np.asarray(K_hat_d, dtype=F32)
+    P_d = np.asarray(P_d, dtype=F32)
+    D = P_d.shape[0]
+    q_hat_d = (q @ P_d).astype(F32)
+    logits = (K @ q_hat_d).astype(F32) / F32(math.sqrt(D))
+    w = softmax_row(logits)
+    return (w @ np.asarray(V, dtype=F32)).astype(F32)
+
+
 # --------------------------------------------------------------------------
 # rotary embedding  (rope.py)
 # --------------------------------------------------------------------------
@@ -330,6 +389,26 @@ def tie_band(q_hat, K_hat, d: int, k: int) -> np.ndarray:
     jstar = order[k - 1]
     T = a64[jstar]
     return np.abs(a64 - T) <= 2.0 * (tau + tau[jstar])
+
+
+def tie_band_shared(q_block, K_hat, d: int, k: int) -> np.ndarray:
+    """Tie band of the group-shared selection: the group score sum_g q_g . K_j[:d] is
+    computed either as a sum of G per-head fp32 dots (the reference composition) or as
+    one dot with the fp32-summed query (the kernel); both are within
+    gamma_{d+G} sum_g sum_t |q_gt K_jt| of the exact value."""
+    Q = np.asarray(q_block, dtype=F64).reshape(-1, np.shape(K_hat)[1])[:, :d]
+    K = np.asarray(K_hat, dtype=F64)[:, :d]
+    a64 = K @ Q.sum(axis=0)
+    S = a64.size
+    if k >= S:
+        return np.zeros(S, dtype=bool)
+    u = 2.0 ** -24
+    n = d + Q.shape[0]
+    gamma = n * u / (1.0 - n * u)
+    tau = gamma * (np.abs(K) @ np.abs(Q).sum(axis=0))
+    order = np.argsort(-a64, kind="stable")
+    jstar = order[k - 1]
+    return np.abs(a64 - a64[jstar]) <= 2.0 * (tau + tau[jstar])
 
 
 def sets_match_outside_band(gpu_idx, ref_idx, band) -> bool:

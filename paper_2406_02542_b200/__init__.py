@@ -22,6 +22,7 @@ from .attention import (
     loki_attention,
     loki_decode,
     loki_rank_and_attend,
+    pca_attn,
     resolve_fraction,
     transform_step,
     vanilla_attention,

@@ -246,6 +246,34 @@ def exact_topk_attention(q, K, V, k: int):
     return _core.back(y, host), _core.back(idx.reshape(-1).to(torch.int64), host)
 
 
+def pca_attn(q, K_hat_d, V, P_d):
+    """Attend to every token using only leading-d coordinates (attention.py:209-232): the
+    cache holds K_hat[:, :d]; logits q_hat[:d] . K_hat[j, :d] / sqrt(D) (the full head
+    dimension), softmax over all rows, no selection.  A quality baseline,
+    composed from the device kernels: the query projection (cuBLAS matvec), the sliced
+    score kernel, the fp64 softmax kernel and the dense weighted-sum kernel."""
+    from .kernels import dense_weighted_sum_kernel, sliced_score_kernel
+    from .linalg import softmax_rows
+
+    qt, host = _core.as_device(q, torch.float32)
+    qt = qt.reshape(-1)
+    Kd, _ = _core.as_device(K_hat_d, torch.float32, device=qt.device)
+    Vt, _ = _core.as_device(V, torch.float32, device=qt.device)
+    Pd, _ = _core.as_device(P_d, torch.float32, device=qt.device)
+    if Pd.dim() != 2 or Pd.shape[0] != qt.shape[0]:
+        raise ShapeError(f"P_d shape {tuple(Pd.shape)} does not match query dim {qt.shape[0]}")
+    d = Pd.shape[1]
+    if Kd.dim() != 2 or Kd.shape[1] != d:
+        raise ShapeError(f"reduced keys {tuple(Kd.shape)} do not match P_d width {d}")
+    if Vt.dim() != 2 or Vt.shape[0] != Kd.shape[0] or Vt.shape[0] < 1:
+        raise ShapeError(f"values {tuple(Vt.shape)} do not match keys {tuple(Kd.shape)}")
+    D = Pd.shape[0]
+    q_hat_d = (qt @ Pd).contiguous()
+    logits = sliced_score_kernel(q_hat_d, Kd.contiguous(), d) / np.float32(math.sqrt(D))
+    w = softmax_rows(logits.reshape(1, -1)).reshape(-1)
+    return _core.back(dense_weighted_sum_kernel(w, Vt), host)
+
+
 def loki_rank_and_attend(q_hat, K_hat, V, d: int, k: int):
     """Reduced-dimension top-k step over an existing cache (attention.py:166-185).
 

@@ -53,3 +53,24 @@ def loki_case(golden, i):
 def ragged(golden, prefix, i):
     offs = golden[prefix + "/offsets"]
     return offs[i], offs[i + 1]
+
+
+def shared_case(golden, i):
+    """Inputs of make_golden.shared_cases() case i (same draw order), digest-checked."""
+    S, D, G, d, k, seed = (int(x) for x in golden["shared/cases"][i])
+    rng = np.random.default_rng(seed)
+    Q = rng.standard_normal((G, D)).astype(np.float32)
+    K = rng.standard_normal((S, D)).astype(np.float32)
+    V = rng.standard_normal((S, D)).astype(np.float32)
+    assert digest(Q, K, V) == str(golden[f"shared/{i}/sha"]), "input regeneration drifted"
+    return dict(S=S, D=D, G=G, d=d, k=k, Q=Q, K=K, V=V)
+
+
+def quality_inputs(golden):
+    """Inputs of make_golden.quality_cases() (agreement sweep, pca_attn), digest-checked."""
+    keys = O.gen_synthetic_keys(2048, 64, 8, 1e-2, 21)
+    rng = np.random.default_rng(22)
+    V = rng.standard_normal(keys.shape).astype(np.float32)
+    Q = rng.standard_normal((6, 64)).astype(np.float32)
+    assert digest(keys, V, Q) == str(golden["agree/keys_sha"]), "input regeneration drifted"
+    return keys, V, Q

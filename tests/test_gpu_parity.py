@@ -571,3 +571,38 @@ def test_decode_graph_replay_matches_eager_steps():
         torch.cuda.synchronize()
         for layer, dec in enumerate(decs):
             assert torch.equal(dec.out, eager[layer]), (trial, layer)
+
+
+@pytest.mark.gpu
+def test_agreement_sweep_vs_reference_golden(golden):
+    """N3: the device agreement_sweep against the reference's own metrics.agreement_sweep output
+    (tests/golden/make_golden.py quality_cases: same keys, values, queries and projection)."""
+    from golden_inputs import quality_inputs
+
+    keys, V, Q = quality_inputs(golden)
+    stats = L.agreement_sweep(keys, V, Q, golden["agree/P"], [0.125, 0.25, 0.5], [0.25, 0.5, 1.0])
+    ref = golden["agree/cells"]
+    assert len(stats.cells) == len(ref)
+    S = keys.shape[0]
+    for c, r in zip(stats.cells, ref):
+        assert (c.k_f, c.d_f) == (r[0], r[1])
+        k = L.resolve_fraction(c.k_f, S)
+        # a set can differ only by boundary ties decided by fp32 summation order: one swap moves a
+        # query's Jaccard by at most 2 / k
+        assert abs(c.mean_jaccard - r[2]) <= 2.0 / k, (c, r)
+        assert abs(c.min_jaccard - r[3]) <= 2.0 / k, (c, r)
+
+
+@pytest.mark.gpu
+def test_pca_attn_vs_reference_golden(golden):
+    """N3: pca_attn (attention.py:209-232) on the device against the reference's outputs."""
+    from golden_inputs import quality_inputs
+
+    keys, V, Q = quality_inputs(golden)
+    P = golden["agree/P"]
+    K_hat = (keys @ P).astype(np.float32)
+    for j, d in enumerate(golden["pca_attn/d"]):
+        d = int(d)
+        y = np.stack([L.pca_attn(Q[i], np.ascontiguousarray(K_hat[:, :d]), V, np.ascontiguousarray(P[:, :d]))
+                      for i in range(Q.shape[0])])
+        assert O.rel_err(y, golden["pca_attn/y"][j]) <= 1e-5, d

@@ -157,3 +157,32 @@ def test_decode_graph_validates_before_capture():
     before touching the device (capture itself needs a GPU: test_gpu_parity)."""
     with pytest.raises(L.ShapeError):
         L.DecodeGraph([])
+
+
+def test_formats_byte_identical_to_reference_writers(golden, tmp_path):
+    """N4: LKD1 / LKP1 files written by the reference's own writers (dataio.py:91-222, bytes recorded by
+    tests/golden/make_golden.py) parse here, and this package writes the same bytes back."""
+    import paper_2406_02542_b200 as L
+    from paper_2406_02542_b200 import dataio
+
+    ref_lkd = golden["fmt/lkd_bytes"].tobytes()
+    p = tmp_path / "ref.lkd"
+    p.write_bytes(ref_lkd)
+    hdr, keys = dataio.read_key_dump(str(p))
+    assert (hdr.layer, hdr.head, hdr.seq_len, hdr.head_dim, hdr.rotary_stage) == (3, 5, 40, 16, "post")
+    np.testing.assert_array_equal(keys, golden["fmt/lkd_keys"])
+    q = tmp_path / "ours.lkd"
+    dataio.write_key_dump(str(q), hdr, keys)
+    assert q.read_bytes() == ref_lkd
+
+    ref_lkp = golden["fmt/lkp_bytes"].tobytes()
+    p = tmp_path / "ref.lkp"
+    p.write_bytes(ref_lkp)
+    proj = dataio.read_projection(str(p))
+    assert (proj.layer, proj.head, proj.rotary_stage) == (3, 5, "post")
+    np.testing.assert_array_equal(np.asarray(proj.P), golden["fmt/lkp_P"])
+    np.testing.assert_array_equal(np.asarray(proj.eigenvalues), golden["fmt/lkp_eig"])
+    q = tmp_path / "ours.lkp"
+    dataio.write_projection(str(q), proj)
+    assert q.read_bytes() == ref_lkp
+    assert L.ProjectionSet is type(proj)

@@ -154,3 +154,31 @@ def test_cpu_unit_matches_oracle(golden):
     assert O.rel_err(y, golden["loki/4/y"]) <= 1e-5
     yv = O.dense_unit_cpu(c["q"], c["K"], c["V"])
     assert O.rel_err(yv, golden["loki/4/vanilla_y"]) <= 1e-5
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_shared_selection_vs_reference_composition(golden, i):
+    """The group-shared mode's oracle against the reference primitives composed in make_golden.py."""
+    from golden_inputs import shared_case
+
+    c = shared_case(golden, i)
+    y, idx, group, w = O.loki_rank_and_attend_shared(c["Q"], c["K"], c["V"], c["d"], c["k"])
+    assert O.rel_err(group, golden[f"shared/{i}/group"]) <= 1e-5
+    band = O.tie_band_shared(c["Q"], c["K"], c["d"], c["k"])
+    assert O.sets_match_outside_band(idx, golden[f"shared/{i}/idx"], band)
+    if np.array_equal(idx, golden[f"shared/{i}/idx"]):
+        assert O.rel_err(y, golden[f"shared/{i}/y"]) <= 1e-5
+        assert np.abs(w - golden[f"shared/{i}/weights"]).max() <= 1e-6
+
+
+def test_pca_attn_vs_reference(golden):
+    from golden_inputs import quality_inputs
+
+    keys, V, Q = quality_inputs(golden)
+    P = golden["agree/P"]
+    K_hat = (keys @ P).astype(np.float32)
+    for j, d in enumerate(golden["pca_attn/d"]):
+        d = int(d)
+        y = np.stack([O.pca_attn(Q[i], np.ascontiguousarray(K_hat[:, :d]), V, np.ascontiguousarray(P[:, :d]))
+                      for i in range(Q.shape[0])])
+        assert O.rel_err(y, golden["pca_attn/y"][j]) <= 1e-5, d
