@@ -268,7 +268,14 @@ class Workload:
         self.full_out = torch.empty(L, B, Hq, D, device=dev) if world > 1 else None
 
     def decoders(self, dense=False):
+        """One LokiDecoder per layer (dense: the comparator, writing a scratch output so the Loki
+        outputs in self.out stay what the timed step produced)."""
+        import torch
+
         from paper_2406_02542_b200 import LokiDecoder, _lib
+
+        if dense and getattr(self, "dense_out", None) is None:
+            self.dense_out = torch.empty_like(self.out[0])
 
         decs = []
         for layer in range(self.L):
@@ -276,7 +283,9 @@ class Workload:
                 self.K[layer], self.V[layer], None if dense else self.P[layer], Hq=self.Hq_l, d=self.d,
                 k_f=self.cfg["k_f"], rows=self.rows, lens=self.lens, S_max=self.S, q_raw=self.q_raw[layer],
                 k_raw=self.k_raw[layer], v_new=self.v_new[layer], rope_mode=_lib.ROPE_ROTATE_THEN_PROJECT,
-                rope_base=self.cfg["base"], positions=self.positions, dense=dense, out=self.out[layer]))
+                rope_base=self.cfg["base"], positions=self.positions, dense=dense,
+                out=(self.dense_out if dense else self.out[layer]),
+                group_select=self.cfg.get("group_select", "per_head")))
         return decs
 
 
@@ -585,8 +594,9 @@ def parity_check(wl, dec, n_units=128, seed=321):
     import paper_2406_02542_b200 as L
     from oracle import loki_oracle as O
 
+    shared = wl.cfg.get("group_select") == "shared" and wl.G > 1
     y_diag, diag = L.loki_decode(dec.q_hat, wl.K[0], wl.V[0], wl.lens, d=wl.d, k_f=wl.cfg["k_f"],
-                                 diagnostics=True, S_max=wl.S)
+                                 diagnostics=True, S_max=wl.S, group_select=wl.cfg.get("group_select", "per_head"))
     torch.cuda.synchronize()
     prod_vs_diag = float((y_diag - wl.out[0]).abs().max())
     rng = np.random.default_rng(seed)
@@ -604,9 +614,15 @@ def parity_check(wl, dec, n_units=128, seed=321):
         if (b, g) not in cache:
             cache = {(b, g): (wl.K[0][b, g].float().cpu().numpy(), wl.V[0][b, g].float().cpu().numpy())}
         Kb, Vb = cache[(b, g)]
-        y_ref, ref_idx, _, _ = O.loki_rank_and_attend(q_hat[b, h], Kb, Vb, wl.d, wl.k)
         got = idx[b, h, :wl.k]
-        band = O.tie_band(q_hat[b, h], Kb, wl.d, wl.k)
+        if shared:  # the group's one selection (oracle: reference primitives composed, SURVEY 7 part 3)
+            Qg = q_hat[b, g * wl.G:(g + 1) * wl.G]
+            ys, ref_idx, _, _ = O.loki_rank_and_attend_shared(Qg, Kb, Vb, wl.d, wl.k)
+            y_ref = ys[h - g * wl.G]
+            band = O.tie_band_shared(Qg, Kb, wl.d, wl.k)
+        else:
+            y_ref, ref_idx, _, _ = O.loki_rank_and_attend(q_hat[b, h], Kb, Vb, wl.d, wl.k)
+            band = O.tie_band(q_hat[b, h], Kb, wl.d, wl.k)
         good = O.sets_match_outside_band(got, ref_idx, band) and bool(np.all(np.diff(got) > 0))
         if not np.array_equal(got, ref_idx):
             swaps += 1
@@ -638,7 +654,8 @@ def config_block(cfg, args, world, d, k):
             "rotary": f"pre-rotary PCA, rotate-then-project, base {cfg['base']:g}",
             "l2": "inputs larger than L2 (KV per layer >> 126 MB); no flush",
             "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
-            **({"gqa_queries": cfg.get("gqa_queries", "independent")} if cfg["Hq"] > cfg["Hkv"] else {})}
+            **({"gqa_queries": cfg.get("gqa_queries", "independent"),
+                "group_select": cfg.get("group_select", "per_head")} if cfg["Hq"] > cfg["Hkv"] else {})}
 
 
 def peak_gbs():
@@ -662,7 +679,7 @@ def attention_block(wl, decs, reps, world, with_dense=True):
         attend()
     fused_us = time_region(attend, reps, world) * 1000.0 / (reps * wl.L)
     units = wl.B * wl.Hkv_l
-    U = float(wl.k) if wl.G == 1 else union_rows(wl, decs[0])
+    U = float(wl.k) if (wl.G == 1 or wl.cfg.get("group_select") == "shared") else union_rows(wl, decs[0])
     algo_bytes = metrics.loki_bytes(units, wl.S, wl.D, wl.d, U, 2)
     dense_bytes = metrics.dense_bytes(units, wl.S, wl.D, 2)
     blk = {"loki_attention_us_per_layer": round(fused_us, 3), "algorithmic_bytes_per_layer": int(algo_bytes),
@@ -730,6 +747,92 @@ def gather_compare(wl, dec, reps):
                     "(SELECT_INDICES) vs torch K[idx] / V[idx] copies + SDPA"}
 
 
+def full_model_block(args, steps=8):
+    """BASELINE configs[1] as a whole model: a random-init Llama2-7B (32 layers, hidden 4096, 32 heads,
+    MLP 11008, vocab 32000, bf16) decoding one token for B = 16 sequences of 8192 cached tokens through
+    the HF integration (paper_2406_02542_b200.hf: LokiCache + the "loki" attention), against the same
+    model decoding with exact dense attention (SDPA) over the same rotated cache.  Synthetic caches
+    (make_layer recipe) stand in for a prefill; each step re-decodes the token at row S - 1."""
+    import torch
+
+    from paper_2406_02542_b200 import hf
+
+    try:
+        from transformers import LlamaConfig, LlamaForCausalLM
+    except ImportError as e:  # pragma: no cover
+        return {"error": f"transformers unavailable: {e}"}
+    cfg = dict(CONFIGS["C2"], name="C2")
+    B, S, L, H, D = cfg["B"], cfg["S"], 32, cfg["Hq"], cfg["D"]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    conf = LlamaConfig(vocab_size=32000, hidden_size=4096, intermediate_size=11008, num_hidden_layers=L,
+                       num_attention_heads=H, num_key_value_heads=cfg["Hkv"], head_dim=D,
+                       max_position_embeddings=S + 64, rope_theta=cfg["base"], attn_implementation="sdpa")
+    torch.manual_seed(0)
+    old = torch.get_default_dtype()
+    torch.set_default_dtype(torch.bfloat16)
+    try:
+        with torch.device(dev):
+            model = LlamaForCausalLM(conf).eval()
+    finally:
+        torch.set_default_dtype(old)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(21)
+    Ps, cache = [], None
+    layers = []
+    for _ in range(L):
+        K, V, P = make_layer(cfg, B, cfg["Hkv"], dev, gen)
+        layers.append((K, V))
+        Ps.append(P)
+    cache = hf.LokiCache(Ps)
+    for layer, (K, V) in zip(cache.layers, layers):
+        layer.load(K, V, S - 1)
+    del layers
+    ids = torch.randint(0, conf.vocab_size, (B, 1), device=dev, generator=gen)
+    pos = torch.full((B, 1), S - 1, dtype=torch.long, device=dev)
+
+    def step():
+        cache.set_length(S - 1)  # re-decode the token at row S - 1: every step sees S cached rows
+        return model(input_ids=ids, position_ids=pos, past_key_values=cache, use_cache=True,
+                     logits_to_keep=1).logits
+
+    res = {"workload": "Llama2-7B random-init full-model decode, B=16, S=8192, k_f=d_f=0.25, bf16, "
+                       "HF transformers forward (eager) with hf.LokiCache"}
+    with torch.no_grad():
+        for name, dense in (("loki", False), ("dense_sdpa", True)):
+            hf.install(model, Ps, k_f=cfg["k_f"], d_f=cfg["d_f"], dense=dense)
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ms = time_region(step, steps, 1) / steps
+            wall = (time.perf_counter() - t0) * 1000.0 / steps
+            res[f"{name}_eager_ms_per_token"] = round(ms, 3)
+            res[f"{name}_eager_host_wall_ms_per_token"] = round(wall, 3)
+            # the serving form: the whole forward (embedding -> 32 layers -> logits) as one CUDA graph
+            try:
+                run, mode, g = capture(step)
+                if mode != "cuda-graph":
+                    raise RuntimeError("capture fell back to eager")
+                for _ in range(3):
+                    run()
+                gms = time_region(run, steps, 1) / steps
+                res[f"{name}_graph_ms_per_token"] = round(gms, 3)
+                del g
+            except Exception as e:  # pragma: no cover - depends on the HF forward being capturable
+                log(f"[bench] full-model {name}: CUDA graph capture failed ({e!r}); eager only")
+                gms = None
+            best = gms if gms is not None else ms
+            res[f"{name}_ms_per_token"] = round(best, 3)
+            res[f"{name}_tokens_per_s"] = round(B * 1000.0 / best, 1)
+    res["speedup"] = round(res["dense_sdpa_ms_per_token"] / res["loki_ms_per_token"], 3)
+    res["timing"] = ("CUDA events; *_ms_per_token = the CUDA-graph replay of the HF forward when capturable, "
+                     "else eager (host launch overhead included); both forms reported")
+    del model, cache
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
 def tgt_block(args, world, rank):
     """North-star shape (TGT: MHA 32 heads, B = 16, S = 32K, k_f = d_f = 0.25) measured in the default run:
     Loki attention, its roofline fraction and the speed-up over the fastest dense decode."""
@@ -763,16 +866,23 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline and the parity sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the dense comparators and the TGT block")
     ap.add_argument("--no-tgt", action="store_true")
+    ap.add_argument("--no-full-model", action="store_true", help="skip the HF full-model decode leg")
+    ap.add_argument("--full-model", action="store_true", help="run only the HF full-model decode leg")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--gqa-queries", default="independent", choices=["independent", "correlated"],
                     help="GQA query heads: independent N(0,1), or q_0 + 0.5 eps per group (SURVEY 8(d) M2)")
+    ap.add_argument("--group-select", default="per_head", choices=["per_head", "shared"],
+                    help="GQA selection: per query head (the reference's semantics) or one per KV group "
+                         "on the summed group query (opt-in mode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = dict(CONFIGS[args.config], gqa_queries=args.gqa_queries, name=args.config)
+    cfg = dict(CONFIGS[args.config], gqa_queries=args.gqa_queries, group_select=args.group_select,
+               name=args.config)
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, cfg, int(os.environ.get("WORLD_SIZE", "1")), rank)
@@ -783,6 +893,9 @@ def main():
     import torch
 
     world, rank, local = dist_setup()
+    if args.full_model:
+        print(json.dumps({"full_model": full_model_block(args, steps=max(3, args.steps))}), flush=True)
+        return
     if world != args.gpus and rank == 0:
         log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: measuring {world} rank(s)")
     import paper_2406_02542_b200 as L
@@ -857,9 +970,10 @@ def main():
                "path": e2e_path}
 
     cpu = parity = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_parity:
         # the production step left layer 0's q_hat / output in place: check them against the oracle
         parity = parity_check(wl, decs[0])
+    if rank == 0 and world == 1 and not args.no_cpu:
         units, sampled = cpu_units(cfg, wl.B, wl.Hkv_l)
         host = host_layer(wl.K[0], wl.V[0], wl.P[0], wl.q_raw[0], wl.k_raw[0], units if sampled else None)
         cref = CpuReference(host, cfg, wl.d, wl.k, units)
@@ -878,7 +992,7 @@ def main():
                "spread_us": [round(min(walls) * scale * 1e6, 1), round(max(walls) * scale * 1e6, 1)]}
         del host
 
-    tgt = None
+    tgt = full = None
     if rank == 0 and world == 1 and args.config == "C2" and not (args.no_extras or args.no_tgt):
         del step, g_step
         if e2e is not None:
@@ -887,6 +1001,12 @@ def main():
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         tgt = tgt_block(args, world, rank)
+        if not args.no_full_model:
+            try:
+                full = full_model_block(args)
+            except Exception as e:  # the attention line stands on its own; report why the model leg failed
+                log(f"[bench] full-model leg failed: {e!r}")
+                full = {"error": repr(e)[:300]}
 
     if rank == 0:
         achieved = attn["achieved_gbs"]
@@ -911,6 +1031,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "tgt": tgt,
+            "full_model": full,
             "gpu_launches": (1 + (2 if plan["ctas_per_unit"] == -2 else 1)) * wl_layers(cfg) * args.steps,
             "clocks": clocks_rec,
             "timing": f"{mode}; CUDA events on the launching stream, barrier + sync both sides, max over ranks",

@@ -59,6 +59,14 @@ typedef int32_t loki_status;
 #define LOKI_SELECT_ALL 1      /* attention.py:137-142 vanilla_attention (dense) */
 #define LOKI_SELECT_INDICES 2  /* kernels.py:244-279 gathered score/sum on given indices */
 #define LOKI_SELECT_NONE 3     /* kernels.py:223-241 sliced_score_kernel only    */
+/* Opt-in GQA mode (hard part 3): the Hq/Hkv query heads of a KV group share ONE selection of k
+ * rows, ranked on the group's summed leading-d scores sum_g q_g[:d] . K_hat[j, :d]; every head then
+ * attends over that selection exactly.  Composition of reference primitives: sliced_score_kernel on the
+ * [G, D] query block (kernels.py:223-241) summed over the group -> topk_indices (linalg.py:95-118) ->
+ * per-head attention.py:180-184.  Same as LOKI_SELECT_TOPK when Hq == Hkv.  bf16 caches, TMA-addressable
+ * geometry (else LOKI_ERR_UNSUPPORTED).  Diagnostics: every head of a group reports the same indices
+ * and the group score as its approx_scores. */
+#define LOKI_SELECT_TOPK_SHARED 4
 
 typedef struct loki_kv_geom {
   int32_t B, Hq, Hkv, D, S_cap;

@@ -36,6 +36,7 @@ SELECT_TOPK = 0
 SELECT_ALL = 1
 SELECT_INDICES = 2
 SELECT_NONE = 3
+SELECT_TOPK_SHARED = 4  # opt-in GQA: one selection per KV group on the summed group query
 
 # every symbol include/loki_b200.h declares (checked by tests/test_host.py)
 EXPORTED = (

@@ -372,7 +372,7 @@ def transform_step(q_raw, k_raw, position: int, proj: ProjectionSet, rope_params
 
 
 def loki_decode(q_hat, K_hat, V, lens=None, *, d=None, k=None, k_f=None, cfg: LokiConfig | None = None,
-                diagnostics=False, S_max=None, out=None, cluster=0):
+                diagnostics=False, S_max=None, out=None, cluster=0, group_select="per_head"):
     """Batched Loki decode attention on the device (the north-star hot path).
 
     q_hat [B, Hq, D] fp32 (PCA basis); K_hat / V [B, Hkv, S_cap, D] fp32 or bf16
@@ -383,7 +383,14 @@ def loki_decode(q_hat, K_hat, V, lens=None, *, d=None, k=None, k_f=None, cfg: Lo
     Returns y [B, Hq, D] fp32 and, with diagnostics=True, LokiDiagnostics with
     indices int64 [B, Hq, k_max] (-1 past a row's k), approx_scores
     [B, Hq, S_cap] and weights [B, Hq, k_max].
+
+    group_select (GQA): "per_head" (default, the reference's semantics: every query head ranks
+    and selects on its own scores) or "shared" (opt-in: the heads of a KV group share one
+    selection, ranked on the group's summed leading-d scores -- the composition of the
+    reference's sliced_score_kernel on the [G, D] query block, a sum over the group,
+    topk_indices, then per-head attention; bf16 caches).  The two coincide when Hq == Hkv.
     """
+    mode = _select_mode(group_select)
     q, host = _core.as_device(q_hat, torch.float32)
     K, _ = _core.as_device(K_hat, torch.float32, device=q.device, keep_dtype=True, rows_only=True)
     Vt, _ = _core.as_device(V, torch.float32, device=q.device, keep_dtype=True, rows_only=True)
@@ -429,7 +436,7 @@ def loki_decode(q_hat, K_hat, V, lens=None, *, d=None, k=None, k_f=None, cfg: Lo
         approx = torch.zeros((B, Hq, phys), dtype=torch.float32, device=q.device)
         w = torch.zeros((B, Hq, kmax), dtype=torch.float32, device=q.device)
     call = _core.DecodeCall(q, K, Vt, lens_t, S_max, d, k_f=k_f or 0.0, k_fixed=k or 0,
-                            select_mode=_lib.SELECT_TOPK, idx_stride=kmax, out=y, idx_out=idx,
+                            select_mode=mode, idx_stride=kmax, out=y, idx_out=idx,
                             approx_out=approx, weights_out=w, cluster=cluster)
     call.run()
     if not diagnostics:
@@ -438,6 +445,14 @@ def loki_decode(q_hat, K_hat, V, lens=None, *, d=None, k=None, k_f=None, cfg: Lo
                            approx_scores=_core.back(approx[..., :S_cap], host),
                            weights=_core.back(w, host))
     return _core.back(y, host), diag
+
+
+def _select_mode(group_select) -> int:
+    if group_select == "per_head":
+        return _lib.SELECT_TOPK
+    if group_select == "shared":
+        return _lib.SELECT_TOPK_SHARED
+    raise DomainError(f"group_select must be 'per_head' or 'shared', got {group_select!r}")
 
 
 def dense_decode(q, K, V, lens=None, *, S_max=None, out=None, cluster=0):
@@ -472,7 +487,8 @@ class LokiDecoder:
     """
 
     def __init__(self, K, V, P, *, Hq, d, k_f=None, k=None, rows, lens, S_max=None, q_raw, k_raw, v_new,
-                 rope_mode=_lib.ROPE_NONE, rope_base=10000.0, positions=None, dense=False, out=None, cluster=0):
+                 rope_mode=_lib.ROPE_NONE, rope_base=10000.0, positions=None, dense=False, out=None, cluster=0,
+                 group_select="per_head"):
         self.device = K.device
         self.lib = _lib.lib_for(self.device)
         self.K, self.V, self.P = K, V, P
@@ -491,7 +507,8 @@ class LokiDecoder:
         if not 1 <= S_max <= K.shape[2]:
             raise ShapeError(f"S_max {S_max} outside [1, {K.shape[2]}]")
         self.call = _core.DecodeCall(self.q_hat, K, V, lens, S_max, d, k_f=k_f or 0.0, k_fixed=k or 0,
-                                     select_mode=_lib.SELECT_ALL if dense else _lib.SELECT_TOPK, out=self.out,
+                                     select_mode=_lib.SELECT_ALL if dense else _select_mode(group_select),
+                                     out=self.out,
                                      Hq=Hq, cluster=cluster)
 
     def append(self, stream):

@@ -67,9 +67,11 @@ loki_status validate(const loki_decode_args* a) {
   if (a->S_max < 1) return fail(LOKI_ERR_SHAPE, "attention needs at least one cached token");
   if (a->S_max > g.S_cap) return fail(LOKI_ERR_SHAPE, "S_max %d exceeds cache capacity %d", a->S_max, g.S_cap);
   if (a->lens == nullptr) return fail(LOKI_ERR_SHAPE, "lens is required");
-  if (a->select_mode < 0 || a->select_mode > 3) return fail(LOKI_ERR_DOMAIN, "select_mode %d", a->select_mode);
-  const bool computes_scores = a->ext_scores == nullptr &&
-                               (a->select_mode == LOKI_SELECT_TOPK || a->select_mode == LOKI_SELECT_NONE);
+  if (a->select_mode < 0 || a->select_mode > 4) return fail(LOKI_ERR_DOMAIN, "select_mode %d", a->select_mode);
+  const bool ranks = a->select_mode == LOKI_SELECT_TOPK || a->select_mode == LOKI_SELECT_TOPK_SHARED;
+  if (a->select_mode == LOKI_SELECT_TOPK_SHARED && a->ext_scores != nullptr)
+    return fail(LOKI_ERR_UNSUPPORTED, "group-shared selection ranks its own approximate scores");
+  const bool computes_scores = a->ext_scores == nullptr && (ranks || a->select_mode == LOKI_SELECT_NONE);
   const bool attends = a->out != nullptr;
   if (computes_scores || attends) {
     if (a->q_hat == nullptr || a->K == nullptr) return fail(LOKI_ERR_SHAPE, "q_hat and K are required");
@@ -90,7 +92,7 @@ loki_status validate(const loki_decode_args* a) {
     return fail(LOKI_ERR_SHAPE, "scores-only call cannot attend");
   if (a->select_mode == LOKI_SELECT_INDICES && a->ext_idx == nullptr)
     return fail(LOKI_ERR_SHAPE, "external index lists are required");
-  if (a->select_mode == LOKI_SELECT_TOPK && !attends && a->idx_out == nullptr && a->approx_out == nullptr)
+  if (ranks && !attends && a->idx_out == nullptr && a->approx_out == nullptr)
     return fail(LOKI_ERR_SHAPE, "ranking-only call without outputs");
   const bool needs_stride = a->ext_idx || a->idx_out || a->weights_out;
   if (needs_stride) {
@@ -244,6 +246,9 @@ struct PipePlan {
   loki::PipeParams p{};
   TmaGeom tg{};
   int G_T = 1;
+  int G_Ta = 1;  // group size the A launch is instantiated for (1 for group-shared selection)
+  loki::PipeParams blay{};  // group-shared: the B-only launch's shared-memory layout (no histogram)
+  size_t smem_b = 0;
   bool big = false;
   bool split = false;  // A-only launch + B-only launch (MHA bf16)
   bool ws_select = false;  // the A launch is the warp-specialised pipe_select_kernel (layout in sel_layout)
@@ -254,7 +259,7 @@ struct PipePlan {
   size_t smem = 0;
   size_t ws = 0;
   size_t off_hist = 0, off_keys = 0, off_tcs = 0, off_poff = 0, off_part = 0, off_spec = 0, off_logits = 0;
-  size_t off_loff = 0;
+  size_t off_loff = 0, off_ml = 0;
 };
 
 // The persistent pipelined kernel (loki_pipe.cu) serves the attending TOPK
@@ -264,10 +269,30 @@ bool pipe_eligible(const loki_decode_args* a) {
   const int G_T = loki::next_pow2(g.Hq / g.Hkv);
   const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   const loki::RowSpace rs = loki::row_space(g);
-  return env_int("LOKI_PIPE", 1) != 0 && a->select_mode == LOKI_SELECT_TOPK && a->ext_scores == nullptr &&
+  return env_int("LOKI_PIPE", 1) != 0 &&
+         (a->select_mode == LOKI_SELECT_TOPK || a->select_mode == LOKI_SELECT_TOPK_SHARED) && a->ext_scores == nullptr &&
          a->out != nullptr && a->K != nullptr && a->V != nullptr && rs.ok && aligned(a->K, 16) &&
          aligned(a->V, 16) && (g.stride_s * e) % 16 == 0 &&
          a->S_max < (1 << 24) && loki::pipe_supported(g.dtype, g.D, G_T) && a->cluster_override == 0;
+}
+
+loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl);
+
+// Group-shared selection with one query head per KV head is plain per-head selection; with groups it
+// exists only on the pipe path (no cluster-kernel fallback).
+const loki_decode_args* canonical_mode(const loki_decode_args* a, loki_decode_args* tmp) {
+  if (a->select_mode != LOKI_SELECT_TOPK_SHARED || a->g.Hq != a->g.Hkv) return a;
+  *tmp = *a;
+  tmp->select_mode = LOKI_SELECT_TOPK;
+  return tmp;
+}
+
+loki_status shared_unsupported(const loki_decode_args* a) {
+  if (!pipe_eligible(a))
+    return fail(LOKI_ERR_UNSUPPORTED, "group-shared selection needs a TMA-addressable cache (16 B aligned rows)");
+  PipePlan pl;
+  const loki_status s = make_pipe_plan(a, &pl);
+  return s != LOKI_OK ? s : fail(LOKI_ERR_UNSUPPORTED, "group-shared selection: no pipe plan");
 }
 
 loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
@@ -277,6 +302,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   const int units = g.B * g.Hkv;
   const int e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   pl->G_T = G_T;
+  const bool shared = a->select_mode == LOKI_SELECT_TOPK_SHARED;  // (G > 1: canonical_mode maps G == 1 to TOPK)
+  if (shared && g.dtype != LOKI_DTYPE_BF16) return fail(LOKI_ERR_UNSUPPORTED, "group-shared selection needs bf16 caches");
   // tensor-core phase 3 (bf16): 16-row stages of K and V (64 * D bytes)
   const bool mma = g.dtype == LOKI_DTYPE_BF16;  // bf16 caches: tensor-core phase 3 (compiled in, not optional)
   const int stage = mma ? 32 * g.D : env_int("LOKI_PIPE_STAGE_KB", 4) * 1024;
@@ -295,7 +322,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // for d = 32 of D = 128 (128 B + 64 B K pieces); the partial scores take Lc words of shared memory per
   // head, so not with the 8192-row chunks
   // (r01: no gain on the tensor-core path at C2, 210.5 vs 211.3 us, and 16 KB more smem: opt-in there)
-  p.split_k = env_int("LOKI_SPLITK", mma ? 0 : 1) != 0 && d < g.D &&
+  p.shared = shared ? G : 0;
+  p.split_k = !shared && env_int("LOKI_SPLITK", mma ? 0 : 1) != 0 && d < g.D &&
               (mma ? (d == 32 && g.D == 128 && G_T <= 4) : (d % vec == 0 && ((g.D - d) * e) % 32 == 0));
   if (mma) p.r3 = 8;
   // one lane per lead row when the row is a TMA swizzle span (64 / 128 B) and r1 covers whole lanes
@@ -312,7 +340,12 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   pl->big = G_T == 1 && env_int("LOKI_PIPE_BIG", a->S_max >= 16384 ? 1 : 0) != 0;
   if (pl->big && mma) p.split_k = 0;
   const int kNB = loki::pipe_blocks_per_warp(G_T, pl->big);
-  const int Lc = kNB * 128 * loki::pipe_warps();
+  int Lc = kNB * 128 * loki::pipe_warps();
+  // group-shared selection publishes entry lists (unless diagnostic weights need the key path): B parts
+  // then copy their slice instead of re-deriving it from the keys, so their size is free of the key-scan
+  // register arrays -- MHA-sized parts (a k-fraction of the rows is selected, whatever the group size)
+  const bool shared_lists = shared && env_int("LOKI_GLOBAL_LISTS", 1) != 0;
+  if (shared_lists) Lc = env_int("LOKI_LISTS_LC", a->S_max >= 16384 ? 8192 : 4096);
   if (Lc % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", Lc, p.r1);
   p.Lc = Lc;
   p.nA = loki::ceil_div(a->S_max, Lc);
@@ -326,6 +359,11 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   p.spec = env_int("LOKI_SPEC", 0) != 0 && G_T <= 4 && a->idx_out == nullptr && p.La == p.Lc;  // opt-in (net loss)
   p.ccap = a->S_max / 4 > 2048 ? a->S_max / 4 : 2048;
   pl->smem = loki::pipe_layout(G_T, &p);
+  if (shared) {  // the B-only launch keeps no histogram: its own, smaller layout (room for the larger parts)
+    pl->blay = p;
+    pl->blay.hbits = 0;
+    pl->smem_b = loki::pipe_layout(G_T, &pl->blay);
+  }
   const size_t ring = (size_t)loki::pipe_warps() * p.nst * p.stage_bytes;
   if ((size_t)loki::pipe_warps() * G_T * (g.D + 2) * 4 > ring || p.cand_cap < 256)
     return fail(LOKI_ERR_UNSUPPORTED, "pipe: ring of %zu bytes too small", ring);
@@ -335,17 +373,20 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // r01: split layers beat the single launch on MHA bf16 (C2 212 -> 205 us, TGT 626 -> 603 us)
   // (short sequences keep one launch: S = 4K 125 vs 137 us split)
   // (r01: GQA too, C3 866 -> 742, C4 989 -> 875, C5s 4445 -> 3468 us)
-  pl->split = env_int("LOKI_PIPE_SPLIT", a->S_max >= 8192 ? 1 : 0) != 0 && g.dtype == LOKI_DTYPE_BF16 && !p.spec;
+  pl->split = (shared || env_int("LOKI_PIPE_SPLIT", a->S_max >= 8192 ? 1 : 0) != 0) && g.dtype == LOKI_DTYPE_BF16 &&
+              !p.spec;
+  pl->G_Ta = shared ? 1 : G_T;  // group-shared: the A launch ranks once per unit (a G = 1 problem)
   if (pl->split) {  // the A-only launch needs no B-item entry region
     pl->smem1 = (size_t)p.off_ents + 1024;
-    const int occ1 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem1, pl->big, 1);
-    const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem, pl->big, 2);
+    const int occ1 = loki::pipe_ctas_per_sm(g.dtype, g.D, pl->G_Ta, pl->smem1, pl->big, 1);
+    const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, shared ? pl->smem_b : pl->smem, pl->big, 2);
     if (occ1 < 1 || occ2 < 1) pl->split = false;
     // A chunks of >= 8192 rows (r01: C2 197.9 -> 193.0 us); the A launch has no lag to feed.  Groups of 8:
     // >= 32768 rows (fewer arrivals into the serial 8-head selection; r01 C5s 3398 -> 3232 us,
     // tools/c5s_sweep.sh).  Groups of 4: >= 16384 rows once the units alone fill an A wave (C4 877 -> 863 us,
     // tools/la_big.sh; C3, 256 units, loses 1.2 % with them and keeps 8192)
-    const int la_min = G_T == 8 ? 32768 : (G_T == 4 && units >= sm_count() * occ1 ? 16384 : 8192);
+    const int GA = pl->G_Ta;
+    const int la_min = GA == 8 ? 32768 : (GA == 4 && units >= sm_count() * occ1 ? 16384 : 8192);
     if (env_int("LOKI_PIPE_LA", 0) == 0 && p.La < la_min) {
       p.La = la_min;
       p.nAa = loki::ceil_div(a->S_max, p.La);
@@ -368,7 +409,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // 209 -> 176 us).  MHA: at most 8 chunks per unit (B = 1, S = 32K: 16 chunks 144 us vs 138 at 4)
   if (env_int("LOKI_PIPE_LA", 0) == 0) {
     const long long target = pl->split ? (long long)pl->grid1 : 128;
-    while ((long long)units * p.nAa < target && p.La >= 2048 && (p.La / 2) % p.r1 == 0 && (G > 1 || p.nAa < 8)) {
+    while ((long long)units * p.nAa < target && p.La >= 2048 && (p.La / 2) % p.r1 == 0 &&
+           (pl->G_Ta > 1 || p.nAa < 8)) {
       p.La /= 2;
       p.nAa = loki::ceil_div(a->S_max, p.La);
     }
@@ -377,9 +419,11 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // histogram merge, no L2 key re-stream; B items copy their slice).  Needs the unit's keys on chip next
   // to the ring: the A-only launch of a split layer carries them in place of the B-entry region
   p.lists = 0;
-  if (pl->split && G_T == 1 && !p.spec && !p.split_k && a->idx_out == nullptr &&
-      a->weights_out == nullptr && (p.lead_swz == 64 || p.lead_swz == 128) && env_int("LOKI_SELECT_WS", 1) != 0 &&
-      units >= sm_count()) {
+  // group-shared selection always runs here: its selection is a G = 1 problem on the summed query (one lane
+  // per lead row, so the G = 1 box rule applies), whatever the number of units
+  const bool g1_lead = (p.lead_swz == 64 || p.lead_swz == 128) && p.r1 % (p.lead_swz == 64 ? 64 : 32) == 0;
+  if (pl->split && (G_T == 1 || shared) && !p.spec && !p.split_k && g1_lead &&
+      env_int("LOKI_SELECT_WS", 1) != 0 && units >= sm_count()) {
     // The warp-specialised A launch (one 16-warp CTA per SM, one whole unit per item): a stream group
     // streams unit i's lead columns while a select group selects unit i - 1, so the selection never
     // idles the loads.  Units of <= 8192 rows keep their keys on chip and publish ordered entry lists
@@ -387,13 +431,24 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
     loki::PipeParams ps = p;
     ps.La = loki::ceil_div(a->S_max, p.r1) * p.r1;
     ps.nAa = 1;
-    const bool onchip = ps.La <= env_int("LOKI_ONCHIP_ROWS", 8192) && ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0;
-    const size_t sw = loki::pipe_select_layout(&ps, onchip);
-    const int ow = sw <= kSmemMax ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, onchip, sw) : 0;
+    // Entry lists need power-of-two half parts; diagnostic weights need the keys left in the workspace
+    // (the merge re-derives each head's selection from them), so such calls keep the key path
+    const bool pow2 = ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0;
+    const bool onchip = ps.La <= env_int("LOKI_ONCHIP_ROWS", 8192) && pow2;
+    // ring stages per stream warp: 3 where they fit (r02: TGT 591 -> 566 us, C2 177 -> 174 us), else 2
+    size_t sw = 0;
+    int ow = 0;
+    for (int nst = env_int("LOKI_SELECT_STAGES", 3); nst >= 2 && ow < 1; --nst) {
+      ps.nst = nst;
+      sw = loki::pipe_select_layout(&ps, onchip);
+      ow = sw <= kSmemMax ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, onchip, sw) : 0;
+    }
     if (ow >= 1) {
       p.La = ps.La;
       p.nAa = 1;
-      p.lists = onchip ? 1 : 0;
+      // (units whose keys stay in the workspace publish lists too: the select group streams them back once
+      // more and writes the entries in place, so B items copy slices instead of re-deriving them)
+      p.lists = (onchip || (pow2 && shared_lists)) ? 1 : 0;
       pl->ws_select = true;
       pl->ws_onchip = onchip;
       pl->sel_layout = ps;
@@ -401,6 +456,10 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
       pl->grid1 = sm_count() * ow;
     }
   }
+  if (shared && !g1_lead)  // (few units: the chunked A-only launch with G = 1 items, MODE 1)
+    return fail(LOKI_ERR_UNSUPPORTED, "group-shared selection: lead rows of %d B in %d-row boxes", p.lead_swz, p.r1);
+  if (shared && !pl->ws_select && shared_lists && ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0)
+    p.lists = 1;  // the last A arriver's selection also emits the unit's entry list (select_unit)
   const size_t kchip = (size_t)G_T * p.La * 4;
   if (!pl->ws_select && pl->split && G_T == 1 && !pl->big && env_int("LOKI_LISTS", 0) != 0 && p.nAa == 1 &&
       !p.spec && !p.split_k && a->idx_out == nullptr && a->weights_out == nullptr &&
@@ -450,6 +509,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   if (a->weights_out != nullptr) off = loki::align_up(off + (size_t)units * G * g.S_cap * 4, 256);
   pl->off_loff = off;
   if (p.lists) off = loki::align_up(off + (size_t)units * (2 * p.nA + 1) * 4, 256);
+  pl->off_ml = off;
+  if (p.lists && a->weights_out != nullptr) off = loki::align_up(off + (size_t)units * G * 2 * 4, 256);
   pl->ws = off;
   return LOKI_OK;
 }
@@ -500,6 +561,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   p.logits = a->weights_out ? reinterpret_cast<float*>(ws + pl.off_logits) : nullptr;
   p.sel = p.lists ? p.keys : nullptr;
   p.loff = p.lists ? reinterpret_cast<uint32_t*>(ws + pl.off_loff) : nullptr;
+  p.ml = (p.lists && a->weights_out) ? reinterpret_cast<float*>(ws + pl.off_ml) : nullptr;
   p.debug = env_int("LOKI_DEBUG", 0);
   p.spin_ns = (long long)env_int("LOKI_SPIN_S", 20) * 1000000000LL;  // sanitizer runs raise it
   p.trace = (loki::g_phase_trace != nullptr && p.n_tickets * 4 <= (long long)loki::g_phase_trace_ctas * 8)
@@ -511,6 +573,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   if (pl.split) {
     loki::PipeParams pa = p, pb = p;
     pa.n_tickets = (long long)p.units * p.nAa;
+    if (p.shared) pa.G = 1;  // the A launch selects once per unit, on the group's summed query
     // units whose B parts run as halves (short drain, opt-in: the grouping of the partial states then
     // depends on the number of units, so KV-head shards would not be bit-identical to one launch)
     int tail = p.halves == 2 ? p.units
@@ -529,17 +592,28 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
       pa.off_kchip = pl.sel_layout.off_kchip;
       pa.off_cand = pl.sel_layout.off_cand;
       pa.cand_bytes = pl.sel_layout.cand_bytes;
+      pa.nst = pl.sel_layout.nst;
       e = loki::launch_pipe_select(pa, g.dtype, pl.ws_onchip, pl.grid1, pl.smem1, maps,
                                    static_cast<cudaStream_t>(stream));
     } else {
-      e = loki::launch_pipe(pa, g.dtype, pl.G_T, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big,
+      e = loki::launch_pipe(pa, g.dtype, pl.G_Ta, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big,
                             p.lists ? 3 : 1);
     }
+    size_t smem2 = pl.smem;
+    if (pl.smem_b > 0) {
+      pb.off_ring = pl.blay.off_ring;
+      pb.off_bars = pl.blay.off_bars;
+      pb.off_hist = pl.blay.off_hist;
+      pb.off_ents = pl.blay.off_ents;
+      smem2 = pl.smem_b;
+    }
     if (e == cudaSuccess)
-      e = loki::launch_pipe(pb, g.dtype, pl.G_T, pl.grid2, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big, 2);
+      e = loki::launch_pipe(pb, g.dtype, pl.G_T, pl.grid2, smem2, maps, static_cast<cudaStream_t>(stream), pl.big, 2);
   } else {
     e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big);
   }
+  if (e == cudaSuccess && p.lists && a->weights_out != nullptr)  // diagnostics: weights from the entry lists
+    e = loki::launch_pipe_weights(p, static_cast<cudaStream_t>(stream));
   if (e == cudaSuccess) e = cudaGetLastError();
   return cuda_status(e, "loki_decode (pipe) launch");
 }
@@ -565,6 +639,8 @@ loki_status loki_device_check(int32_t device) {
 loki_status loki_decode_workspace_bytes(const loki_decode_args* a, size_t* bytes) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
+  loki_decode_args a1;
+  a = canonical_mode(a, &a1);
   {
     PipePlan pl;
     if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {
@@ -572,6 +648,7 @@ loki_status loki_decode_workspace_bytes(const loki_decode_args* a, size_t* bytes
       return LOKI_OK;
     }
   }
+  if (a->select_mode == LOKI_SELECT_TOPK_SHARED) return shared_unsupported(a);
   loki::Plan plan;
   loki::FusedParams p{};
   TmaGeom tg{};
@@ -585,6 +662,8 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
                              size_t* smem_bytes) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
+  loki_decode_args a1;
+  a = canonical_mode(a, &a1);
   PipePlan pl;
   if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {  // persistent grid: 0 (-2: split, two launches)
     if (ctas_per_unit) *ctas_per_unit = pl.split ? -2 : 0;
@@ -592,6 +671,7 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
     if (smem_bytes) *smem_bytes = pl.smem;
     return LOKI_OK;
   }
+  if (a->select_mode == LOKI_SELECT_TOPK_SHARED) return shared_unsupported(a);
   loki::Plan plan;
   loki::FusedParams p{};
   TmaGeom tg{};
@@ -606,10 +686,13 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
 loki_status loki_decode(const loki_decode_args* a, void* stream) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
+  loki_decode_args a1;
+  a = canonical_mode(a, &a1);
   {
     PipePlan pl;
     if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) return run_pipe(a, pl, stream);
   }
+  if (a->select_mode == LOKI_SELECT_TOPK_SHARED) return shared_unsupported(a);
   loki::Plan plan;
   loki::FusedParams p{};
   TmaGeom tg{};

@@ -102,6 +102,11 @@ struct PipeParams {
   int off_cand, cand_bytes;  // warp-specialised A launch: the select group's candidate buffers
   long long spin_ns;  // B items trap after waiting this long for their unit's selection (0: never)
   uint32_t* sel;     // [units][kstride] (aliases keys: lists mode writes no global keys)
+  // group-shared selection (LOKI_SELECT_TOPK_SHARED): the query heads of a KV group share one selection,
+  // made on the group's summed query (sum_g q_g[:d] . K[j, :d]); the A launch runs it as a G = 1 problem
+  // (its params carry G = 1, shared = the group size), the B launch attends every head (full masks)
+  int shared;
+  float* ml;         // [units][G][2] merged (max, sum) per head (lists mode with weights_out only)
   uint32_t* loff;    // [units][2 nA + 1]        // B parts in halves: 2 every unit, 1 tail units only (grouping then depends on #units), 0 none
 };
 
@@ -184,6 +189,7 @@ int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode 
 // layout offsets in *p (ring, bars, double-buffered histograms, on-chip keys or the key stream's buffers,
 // candidates) and returns its bytes.  onchip: keys on chip + lists mode; else keys in the workspace
 size_t pipe_select_layout(PipeParams* p, bool onchip);
+cudaError_t launch_pipe_weights(const PipeParams& p, cudaStream_t st);
 int pipe_select_ctas_per_sm(int dtype, int lead_rb, bool onchip, size_t smem);
 cudaError_t launch_pipe_select(const PipeParams& p, int dtype, bool onchip, int grid, size_t smem,
                                const TmaDesc* maps, cudaStream_t st);

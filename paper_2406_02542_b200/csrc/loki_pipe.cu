@@ -121,6 +121,11 @@ cudaError_t launch_pipe_select(const PipeParams& p, int dtype, bool onchip, int 
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_pipe_weights(const PipeParams& p, cudaStream_t st) {
+  pipe_weights_kernel<<<dim3((unsigned)p.units, (unsigned)p.G), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pipe(const PipeParams& p, int dtype, int G_T, int grid, size_t smem, const TmaDesc* maps,
                         cudaStream_t st, bool big, int mode) {
   if (dtype == LOKI_DTYPE_BF16) {

@@ -137,6 +137,24 @@ __device__ __forceinline__ int k_of(const PipeParams& p, int S) {
 }
 
 // Group-wide inclusive scan of one value per thread, in thread order.
+// Query heads of a unit: the group size, also for the A launch of a group-shared layer (whose params
+// carry G = 1 and shared = the group size).
+__device__ __forceinline__ int unit_heads(const PipeParams& p) { return p.shared > 1 ? p.shared : p.G; }
+// Head mask of a selected row in an entry list: every head of the group in shared mode.
+__device__ __forceinline__ unsigned shared_mask(const PipeParams& p) {
+  return p.shared > 1 ? (1u << p.shared) - 1u : 1u;
+}
+
+// Column c of the query that ranks a unit's rows: q_hat[qrow0] itself, or (group-shared selection)
+// q_0 + q_1 + ... + q_{gs-1} summed in that fixed order in fp32.  Out of line: an inlined loop with a
+// runtime trip count inside the callers' unrolled column loops multiplied their code size (r02: the
+// A launch's kernel grew 5x and ran 40 us slower at C2).
+__device__ __noinline__ float group_q(const PipeParams& p, size_t qrow0, int gs, int c) {
+  float a = p.q_hat[qrow0 * p.D + c];
+  for (int g = 1; g < gs; ++g) a += p.q_hat[(qrow0 + g) * p.D + c];
+  return a;
+}
+
 template <typename Grp = CtaGroup>
 __device__ __forceinline__ unsigned block_incl_scan(unsigned v, PipeShared& sh, unsigned* total) {
   const int lane = lane_id(), w = Grp::warp();
@@ -294,6 +312,10 @@ __device__ __forceinline__ void sel_stamp(const PipeParams& p, int u, int k) {
 // once <= 256 remain) and publishes tcs[u][g].  With idx_out it also
 // publishes each part's output offset (rows above the boundary per part +
 // candidates kept).
+template <typename Grp>
+__device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned long long Tc, uint32_t* kbuf,
+                                  uint64_t* sbar, unsigned& sphase, PipeShared& sh);
+
 template <int G_T>
 __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, uint32_t* hist, uint64_t* sbar,
                             unsigned& sphase, PipeShared& sh) {
@@ -313,7 +335,8 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
   for (int g = 0; g < G; ++g) {
     const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
     uint32_t* gh = p.hist + ((size_t)u * G + g) * HB;
-    uint32_t* poff = offsets ? p.poff + ((size_t)u * G + g) * 2 * p.nA : nullptr;  // per half part
+    // per half part; group-shared selection: the one list's offsets serve (and are copied to) every head
+    uint32_t* poff = offsets ? p.poff + ((size_t)u * unit_heads(p) + g) * 2 * p.nA : nullptr;
     KeyStream ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
     if (g == 0) sel_stamp(p, u, 0);
     const bool spec = p.spec && !offsets;
@@ -525,12 +548,19 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
             const unsigned t = __shfl_up_sync(0xffffffffu, x, off);
             if (lane >= off) x += t;
           }
-          if (q < nhp) poff[q] = run + x - v;
+          if (q < nhp) {
+            poff[q] = run + x - v;
+            for (int gg = 1; gg < p.shared; ++gg) poff[(size_t)gg * 2 * p.nA + q] = run + x - v;
+          }
           run += __shfl_sync(0xffffffffu, x, 31);
         }
       }
     }
     __syncthreads();
+  }
+  if (p.lists && G == 1) {  // lists mode (one selection per unit): ordered entries for the B items
+    __syncthreads();
+    emit_lists_global<CtaGroup>(p, u, S, __ldcg(&p.tcs[u]), reinterpret_cast<uint32_t*>(ring), sbar, sphase, sh);
   }
   if (tid == 0) cu[0] = 0u;  // A arrivals: ready for the next launch
   sel_stamp(p, u, 5);
@@ -685,6 +715,14 @@ __device__ void emit_lists(const PipeParams& p, int u, int S, const uint32_t* ks
   unsigned long long Tc[G_T];
 #pragma unroll
   for (int g = 0; g < G_T; ++g) Tc[g] = g < G ? sh.Tc[g] : ~0ull;
+  const unsigned one = G_T == 1 ? shared_mask(p) : 1u;  // G = 1 lists: a selected row serves the whole group
+  // diagnostics (G = 1 lists): entry order is each head's ascending index order
+  int32_t* idx_dst = nullptr;
+  int nh = 0;
+  if (G_T == 1 && p.idx_out != nullptr) {
+    nh = unit_heads(p);
+    idx_dst = p.idx_out + ((size_t)(u / p.Hkv) * p.Hq + (size_t)(u % p.Hkv) * nh) * p.idx_stride;
+  }
   // warp w: rows [r0, r1), 128 per pass (4 per lane, one uint4 of keys per head)
   const int S8 = ceil_div(ceil_div(S > 0 ? S : 1, Grp::kWarps), 128) * 128;
   const int r0 = min(S, w * S8), r1 = min(S, r0 + S8);
@@ -698,7 +736,7 @@ __device__ void emit_lists(const PipeParams& p, int u, int S, const uint32_t* ks
           const uint4 kk = *reinterpret_cast<const uint4*>(ks + (size_t)g * kst + j);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            m[e] |= (j + e < r1 && comp_key(u4_at(kk, e), j + e) >= Tc[g] ? 1u : 0u) << g;
+            m[e] |= (j + e < r1 && comp_key(u4_at(kk, e), j + e) >= Tc[g] ? one : 0u) << g;
         }
       }
     }
@@ -724,6 +762,15 @@ __device__ void emit_lists(const PipeParams& p, int u, int S, const uint32_t* ks
     int wt;
     unsigned at = base + (unsigned)warp_excl_scan(c, &wt);
     if (j < r1 && (j & ((1 << lhs) - 1)) == 0) lo[j >> lhs] = at;  // entries before row j
+    if (idx_dst != nullptr) {  // diagnostics: the same ascending rows, for every head of the unit
+      unsigned a2 = at;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (m[e]) {
+          for (int g = 0; g < nh; ++g) idx_dst[(size_t)g * p.idx_stride + a2] = j + e;
+          ++a2;
+        }
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       if (m[e]) dst[at++] = (m[e] << 24) | (uint32_t)(j + e);
@@ -923,7 +970,8 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
       RingPos q = rp;
       for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
     }
-    const size_t qrow0 = (size_t)b * p.Hq + (size_t)hk * G;
+    const int gs = unit_heads(p);  // G, or the group whose summed query ranks the rows (shared mode, G = 1 here)
+    const size_t qrow0 = (size_t)b * p.Hq + (size_t)hk * gs;
     const int nch1 = p.dbox / VEC;
     const int LPR1 = next_pow2(nch1);
     const int sl = lane % LPR1;
@@ -994,6 +1042,15 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
           const float bq = c1 < p.d ? p.q_hat[qrow0 * p.D + c1] : 0.f;
           q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
         }
+        if (gs > 1) {  // group-shared selection: rank on the group's summed query
+#pragma unroll
+          for (int j = 0; j < Q2; ++j) {
+            const int c0 = 2 * j, c1 = 2 * j + 1;
+            const float a = c0 < p.d ? group_q(p, qrow0, gs, c0) : 0.f;
+            const float bq = c1 < p.d ? group_q(p, qrow0, gs, c1) : 0.f;
+            q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
+          }
+        }
         for (int k = 0; k < mine; ++k, rp.advance(1)) {
           mbar_wait(&wbar[rp.slot], rp.phase);
           const uint8_t* tile = wring + rp.slot * SB;
@@ -1029,6 +1086,12 @@ __device__ int item_A(const PipeParams& p, const CUtensorMap* lead_map, int u, i
     }
   }
   __syncthreads();
+  if (p.shared > 1 && p.approx_out != nullptr && n > 0) {  // diagnostics: every head reports the group score
+    const size_t r0 = ((size_t)b * p.Hq + (size_t)hk * p.shared) * p.S_cap + row0;
+    for (int g = 1; g < p.shared; ++g)
+      for (int j = tid; j < n; j += kPT) p.approx_out[r0 + (size_t)g * p.S_cap + j] = p.approx_out[r0 + j];
+    __syncthreads();
+  }
   if (p.spec && n > 0) {
     // Speculative candidates (SURVEY 8(a) R7 made cheap): this chunk is a sample of the unit, so the
     // unit's boundary bin is near the chunk's own k * n / S quantile.  Rows within kSpecW bins of
@@ -1119,11 +1182,18 @@ __device__ void merge_unit(const PipeParams& p, int u, int S, PipeShared& sh) {
     }
   }
   __syncthreads();
-  if (p.weights_out != nullptr) {  // softmax weights of each head's selection, ascending rows
+  if (p.weights_out != nullptr && p.lists) {  // lists mode: pipe_weights_kernel finishes the weights
+    if (tid < G) {
+      p.ml[((size_t)u * G + tid) * 2] = sh.gm[tid];
+      p.ml[((size_t)u * G + tid) * 2 + 1] = sh.gl[tid];
+    }
+  } else if (p.weights_out != nullptr) {  // softmax weights of each head's selection, ascending rows
     const unsigned lt = (1u << lane) - 1u;
+    const int Gk = (G_T > 1 && p.shared > 1) ? 1 : G;  // group-shared: one key array and threshold per unit
     for (int g = 0; g < G; ++g) {
-      const unsigned long long Tc = __ldcg(&p.tcs[(size_t)u * G + g]);
-      const uint32_t* keys = p.keys + ((size_t)u * G + g) * p.kstride;
+      const int gk = Gk == 1 ? 0 : g;
+      const unsigned long long Tc = __ldcg(&p.tcs[(size_t)u * Gk + gk]);
+      const uint32_t* keys = p.keys + ((size_t)u * Gk + gk) * p.kstride;
       const float M = sh.gm[g], invL = 1.f / sh.gl[g];
       const float* lg = p.logits + ((size_t)u * G + g) * p.S_cap;
       float* dst = p.weights_out + (qrow0 + g) * p.idx_stride;
@@ -1583,10 +1653,12 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
     const uint32_t* src = p.sel + (size_t)u * p.kstride + e0;
     for (int i = tid; i < n; i += kPT) ents[i] = __ldcg(&src[i]);
   } else if (nrows > 0) {
-    const uint32_t* kbase = p.keys + (size_t)u * G * p.kstride;
+    // group-shared selection: one key array and one threshold per unit; a selected row serves every head
+    const int Gk = (G_T > 1 && p.shared > 1) ? 1 : G;
+    const uint32_t* kbase = p.keys + (size_t)u * Gk * p.kstride;
     unsigned long long Tc[G_T];
 #pragma unroll
-    for (int g = 0; g < G_T; ++g) Tc[g] = g < G ? __ldcg(&p.tcs[(size_t)u * G + g]) : ~0ull;
+    for (int g = 0; g < G_T; ++g) Tc[g] = g < Gk ? __ldcg(&p.tcs[(size_t)u * Gk + g]) : ~0ull;
     const int wr0 = row0 + w * kNB * 128;  // this warp's rows [wr0, wr0 + kNB * 128)
     const int rend = row0 + nrows;
     uint4 kk[kNB][G_T];
@@ -1595,7 +1667,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
       const int jb = wr0 + bq * 128 + 4 * lane;
 #pragma unroll
       for (int g = 0; g < G_T; ++g)
-        kk[bq][g] = (g < G && jb < rend) ? ld_keys4(kbase + (size_t)g * p.kstride, jb) : make_uint4(0u, 0u, 0u, 0u);
+        kk[bq][g] = (g < Gk && jb < rend) ? ld_keys4(kbase + (size_t)g * p.kstride, jb) : make_uint4(0u, 0u, 0u, 0u);
     }
     unsigned m[kNB][4];
     int ns = 0;
@@ -1607,7 +1679,8 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
         unsigned mm = 0;
 #pragma unroll
         for (int g = 0; g < G_T; ++g)
-          if (g < G && j < rend && comp_key(u4_at(kk[bq][g], e), j) >= Tc[g]) mm |= 1u << g;
+          if (g < Gk && j < rend && comp_key(u4_at(kk[bq][g], e), j) >= Tc[g]) mm |= 1u << g;
+        if (G_T > 1 && Gk != G && mm) mm = (1u << G) - 1u;
         m[bq][e] = mm;
         ns += mm != 0;
       }
@@ -2047,7 +2120,85 @@ __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, ui
     }
     sel_stamp<Grp>(p, u, 3);
   }
+  if (p.poff != nullptr && !p.lists) {  // diagnostics (key path): each half part's offset into the index lists
+    const int half = p.Lc / 2, nh = 2 * p.nA;
+    uint32_t* cnt = h;  // the histogram is free again
+    for (int i = tid; i < nh; i += Grp::kThreads) cnt[i] = 0u;
+    Grp::sync();
+    if (kb >= S) {
+      for (int i = tid; i < nh; i += Grp::kThreads) cnt[i] = (unsigned)max(0, min(S - i * half, half));
+    } else if (kb > 0) {
+      ks.start();
+      ks.run([&](int j0, const uint32_t* kc, int nrow) {
+        for (int i = tid; i < nrow; i += Grp::kThreads)
+          if (comp_key(kc[i], j0 + i) >= Tc) atomicAdd(&cnt[(j0 + i) / half], 1u);
+      });
+    }
+    Grp::sync();
+    if (tid == 0) {
+      const int gs = unit_heads(p);
+      unsigned run = 0;
+      for (int i = 0; i < nh; ++i) {
+        for (int g = 0; g < gs; ++g) p.poff[((size_t)u * gs + g) * nh + i] = run;
+        run += cnt[i];
+      }
+    }
+    Grp::sync();
+  }
   if (tid == 0) p.tcs[u] = Tc;
+  Grp::sync();
+}
+
+// Ordered emission (lists mode) for a unit whose keys are in the L2-resident workspace: the keys stream
+// back through the group's two chunk buffers; every selected row (composite key >= Tc) becomes an
+// entry (head mask << 24 | row), ascending, written IN PLACE over the keys (an entry's position never
+// exceeds its row, and rows are consumed chunk by chunk ahead of the writes; the chunks in flight lie
+// past every position written), plus each half part's entry offset in p.loff[u] and, for diagnostics,
+// the heads' ascending index rows.  One selection per unit: G = 1, or group-shared (every head's mask).
+template <typename Grp>
+__device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned long long Tc, uint32_t* kbuf,
+                                  uint64_t* sbar, unsigned& sphase, PipeShared& sh) {
+  constexpr int PER = kCK / Grp::kThreads;  // contiguous keys per thread and chunk
+  const int tid = Grp::tid();
+  const int lhs = 31 - __clz(p.Lc / 2);     // Lc / 2 is a power of two (>= PER)
+  uint32_t* keys = p.keys + (size_t)u * p.kstride;
+  uint32_t* lo = p.loff + (size_t)u * (2 * p.nA + 1);
+  const unsigned full = shared_mask(p) << 24;
+  int32_t* idx_dst = nullptr;
+  int nh = 0;
+  if (p.idx_out != nullptr) {
+    nh = unit_heads(p);
+    idx_dst = p.idx_out + ((size_t)(u / p.Hkv) * p.Hq + (size_t)(u % p.Hkv) * nh) * p.idx_stride;
+  }
+  unsigned base = 0;
+  if (S > 0) {
+    const KeyStreamG<Grp> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
+    ks.start();
+    ks.run([&](int j0, const uint32_t* kc, int nrow) {
+      const int t0 = tid * PER;
+      unsigned m = 0;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        const int j = t0 + e;
+        m |= (j < nrow && comp_key(kc[j], j0 + j) >= Tc ? 1u : 0u) << e;
+      }
+      const unsigned c = __popc(m);
+      unsigned tot;
+      unsigned at = base + block_incl_scan<Grp>(c, sh, &tot) - c;
+      const int r0 = j0 + t0;
+      if (t0 < nrow && (r0 & ((1 << lhs) - 1)) == 0) lo[r0 >> lhs] = at;  // entries before row r0
+#pragma unroll
+      for (int e = 0; e < PER; ++e)
+        if ((m >> e) & 1u) {
+          if (idx_dst != nullptr)
+            for (int g = 0; g < nh; ++g) idx_dst[(size_t)g * p.idx_stride + at] = r0 + e;
+          keys[at++] = full | (uint32_t)(r0 + e);
+        }
+      base += tot;
+    });
+  }
+  if (tid == 0)
+    for (int q = S > 0 ? ((S + (1 << lhs) - 1) >> lhs) : 0; q <= 2 * p.nA; ++q) lo[q] = base;
   Grp::sync();
 }
 
@@ -2149,14 +2300,24 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
           RingPos q = rp;
           for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
         }
-        const size_t qrow0 = (size_t)bb * p.Hq + (size_t)hk;
+        const int gs = unit_heads(p);  // 1, or the group whose summed query ranks the rows (shared mode)
+        const size_t qrow0 = (size_t)bb * p.Hq + (size_t)hk * gs;
         unsigned long long q2[Q2];
 #pragma unroll
-        for (int j = 0; j < Q2; ++j) {
+        for (int j = 0; j < Q2; ++j) {  // (independent loads, all in flight together)
           const int c0 = 2 * j, c1 = 2 * j + 1;
           const float a = c0 < p.d ? p.q_hat[qrow0 * p.D + c0] : 0.f;
           const float bq = c1 < p.d ? p.q_hat[qrow0 * p.D + c1] : 0.f;
           q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
+        }
+        if (gs > 1) {  // group-shared selection: rank on the group's summed query
+#pragma unroll
+          for (int j = 0; j < Q2; ++j) {
+            const int c0 = 2 * j, c1 = 2 * j + 1;
+            const float a = c0 < p.d ? group_q(p, qrow0, gs, c0) : 0.f;
+            const float bq = c1 < p.d ? group_q(p, qrow0, gs, c1) : 0.f;
+            q2[j] = pk2(__float_as_uint(a), __float_as_uint(bq));
+          }
         }
         float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap : nullptr;
         for (int k = 0; k < mine; ++k, rp.advance(1)) {
@@ -2170,6 +2331,11 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
         }
       }
       StreamGrp::sync();  // every key and histogram count of this unit is in shared memory
+      if (p.approx_out != nullptr && p.shared > 1) {  // diagnostics: each head of the group reports the group score
+        const size_t r0 = ((size_t)bb * p.Hq + (size_t)hk * p.shared) * p.S_cap;
+        for (int g = 1; g < p.shared; ++g)
+          for (int j = tid; j < n; j += kPT) p.approx_out[r0 + (size_t)g * p.S_cap + j] = p.approx_out[r0 + j];
+      }
       if (tid == 0) {
         item_u[b] = u;
         mbar_arrive(&full[b]);  // release: the select group acquires through the barrier phase
@@ -2195,6 +2361,7 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       } else {
         select_global<SelectGrp>(p, u, S, hist2 + (size_t)b * HB, kbuf2, sbar, sphase, cand, p.cand_bytes, sh);
         sel_stamp<SelectGrp>(p, u, 4);
+        if (p.lists) emit_lists_global<SelectGrp>(p, u, S, p.tcs[u], kbuf2, sbar, sphase, sh);
       }
       sel_stamp<SelectGrp>(p, u, 5);
       if (tid == 0) {
@@ -2214,6 +2381,20 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       sel_stamp<SelectGrp>(p, u, 6);
     }
   }
+}
+
+// LokiDiagnostics.weights of a lists-mode launch (one selection per unit: G = 1 or group-shared): entry i
+// of unit u is row sel[u][i] for every head, weight exp2(logit - M) / L with the head's merged (M, L).
+// Diagnostics only: a separate small launch keeps this code out of the B items' register budget.
+__global__ void __launch_bounds__(256) pipe_weights_kernel(const PipeParams p) {
+  const int u = blockIdx.x, g = blockIdx.y;
+  const uint32_t* sel = p.sel + (size_t)u * p.kstride;
+  const int total = (int)p.loff[(size_t)u * (2 * p.nA + 1) + 2 * p.nA];
+  const float M = p.ml[((size_t)u * p.G + g) * 2], invL = 1.f / p.ml[((size_t)u * p.G + g) * 2 + 1];
+  const float* lg = p.logits + ((size_t)u * p.G + g) * p.S_cap;
+  const size_t qrow = (size_t)(u / p.Hkv) * p.Hq + (size_t)(u % p.Hkv) * p.G + g;
+  float* dst = p.weights_out + qrow * p.idx_stride;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) dst[i] = exp2f(lg[sel[i] & 0xFFFFFFu] - M) * invL;
 }
 
 }  // namespace

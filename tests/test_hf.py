@@ -106,3 +106,61 @@ def test_sparse_decode_step_matches_oracle():
     d, k = 32, int(np.floor(0.25 * S + 0.5))
     y_ref, _ = O.loki_decode_batched(q, K, V, [S] * q.shape[0], d, k=k)
     assert O.rel_err(y, y_ref) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_loki_cache_appends_in_place():
+    """N2: decode steps write rows into the preallocated buffers through K0 (no concatenation, no new
+    buffers); the stored row is k . P of the post-RoPE key the model produced."""
+    model = _tiny_llama(2)
+    ids = torch.randint(0, 256, (2, 100), device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
+    with torch.no_grad():
+        P = hf.calibrate(model, ids)
+        hf.install(model, P, k_f=0.25, d_f=0.25)
+        cache = hf.LokiCache(P, capacity=256)
+        logits = model(input_ids=ids, past_key_values=cache, use_cache=True).logits[:, -1]
+        layer = cache.layers[0]
+        kp, vp = layer.Kbuf.data_ptr(), layer.Vbuf.data_ptr()
+        for _ in range(4):
+            logits = model(input_ids=logits.argmax(-1, keepdim=True), past_key_values=cache, use_cache=True).logits[:, -1]
+        assert (layer.Kbuf.data_ptr(), layer.Vbuf.data_ptr()) == (kp, vp)
+        assert cache.get_seq_length() == 104 and layer.capacity == 256
+        assert int(layer.lens[0]) == 104
+        # growth past the capacity doubles the buffers and keeps the rows
+        before = layer.Kbuf[:, :, :104].clone()
+        cache2 = hf.LokiCache(P, capacity=16)
+        model(input_ids=ids, past_key_values=cache2, use_cache=True)
+        assert cache2.layers[0].capacity >= 100
+    assert torch.equal(layer.Kbuf[:, :, :104], before)
+
+
+@pytest.mark.gpu
+def test_chunked_prefill_matches_one_prefill():
+    """A second prefill chunk on a non-empty cache sees the cached rows (bottom-right causal mask,
+    ADVICE r01): chunked and one-shot prefill give the same logits."""
+    model = _tiny_llama(2)
+    ids = torch.randint(0, 256, (2, 96), device="cuda", generator=torch.Generator(device="cuda").manual_seed(6))
+    with torch.no_grad():
+        P = hf.calibrate(model, ids)
+        hf.install(model, P, k_f=0.25, d_f=0.25)
+        one = model(input_ids=ids, past_key_values=hf.LokiCache(P), use_cache=True).logits[:, -8:]
+        c = hf.LokiCache(P)
+        model(input_ids=ids[:, :64], past_key_values=c, use_cache=True)
+        two = model(input_ids=ids[:, 64:], past_key_values=c, use_cache=True).logits[:, -8:]
+    rel = (one.float() - two.float()).norm() / one.float().norm()
+    assert rel <= 2e-2, float(rel)
+
+
+@pytest.mark.gpu
+def test_non_default_scale_is_rejected():
+    from paper_2406_02542_b200.errors import UnsupportedShapeError
+
+    model = _tiny_llama(2)
+    ids = torch.randint(0, 256, (1, 40), device="cuda")
+    with torch.no_grad():
+        P = hf.calibrate(model, ids)
+        hf.install(model, P)
+        for m in hf._attention_modules(model):
+            m.scaling = 0.5
+        with pytest.raises(UnsupportedShapeError):
+            model(input_ids=ids, past_key_values=hf.LokiCache(P), use_cache=True)
