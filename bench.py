@@ -708,6 +708,42 @@ def attention_block(wl, decs, reps, world, with_dense=True):
     return blk
 
 
+def phase_split(wl, decs, reps):
+    """Per-phase breakdown (the reference's LOKI_PHASES, bench.py:39): each launch of a layer
+    timed alone with CUDA events, layer by layer as in the step -- K0 ("projection": RoPE, q.P, k.P and the
+    append), the A launch ("approx_scores" + "topk") and the B launch ("exact_scores" + "weighted_sum", with
+    the merge).  Serialised times: in the step the A and B launches overlap (PDL), so their sum exceeds
+    the in-situ attention time."""
+    import torch
+
+    s = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    acc = [0.0, 0.0, 0.0]
+    try:
+        for _ in range(reps):
+            for dec in decs:
+                ev[0].record(s)
+                dec.append(s.cuda_stream)
+                ev[1].record(s)
+                dec.call.run_phase(1, s.cuda_stream)
+                ev[2].record(s)
+                dec.call.run_phase(2, s.cuda_stream)
+                ev[3].record(s)
+                torch.cuda.synchronize()
+                for i in range(3):
+                    acc[i] += ev[i].elapsed_time(ev[i + 1]) * 1000.0
+    except Exception as e:  # single-launch plans have no separate phases
+        return {"error": repr(e)[:200]}
+    n = reps * len(decs)
+    k0, a, b = (x / n for x in acc)
+    return {"projection_append_us": round(k0, 3), "approx_scores_topk_us": round(a, 3),
+            "exact_scores_softmax_wsum_us": round(b, 3), "serialised_sum_us": round(k0 + a + b, 3),
+            "mapping": "projection = K0 (RoPE, q.P, k.P, append); approx_scores + topk = the A launch (leading-d "
+                       "scores, radix selection); exact_scores + weighted_sum = the B launch (gathered exact "
+                       "scores, online softmax, P.V, merge)",
+            "timing": "each launch alone, CUDA events, per layer, mean over all layers x reps"}
+
+
 def gather_compare(wl, dec, reps):
     """R14 / criterion 7 (reference bench.py:275-321, kernels.py:297-308) at layer scale: sparse exact
     attention over a given selection, fused (the library's gather kernel: rows read in place, scores,
@@ -919,9 +955,10 @@ def main():
     reps = max(10, args.steps // 2)
     attn = attention_block(wl, decs, reps, world, with_dense=not args.no_extras)
     fused_us = attn["loki_attention_us_per_layer"]
-    gcmp = None
+    gcmp = phases = None
     if rank == 0 and world == 1 and not args.no_extras:
         gcmp = gather_compare(wl, decs[0], reps)
+        phases = phase_split(wl, decs, 3)
     append_us = max(0.0, us_layer - fused_us)
     peak, peak_src = peak_gbs()
     traffic = None
@@ -1028,6 +1065,7 @@ def main():
                          "rows_gathered_per_unit": attn["rows_gathered_per_unit"]},
             "parity": parity,
             "gather_compare": gcmp,
+            "phases": phases,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "tgt": tgt,

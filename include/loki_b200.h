@@ -114,6 +114,15 @@ loki_status loki_device_check(int32_t device);
  * + weighted-sum chain kernels.py:244-279 / linalg.py:76-92). */
 loki_status loki_decode(const loki_decode_args* args, void* stream);
 
+/* Phase timing: the launches of one loki_decode step separately, for a plan that splits
+ * the layer (S_max >= 8192 bf16, or group-shared selection).  launches = 1: the A launch only (approximate
+ * scores over the leading d columns + the top-k selection, kernels.py:223-241 + linalg.py:95-118);
+ * 2: the B launch only (gathered exact scores, softmax, weighted sum and the merge, kernels.py:244-279 +
+ * linalg.py:76-92) -- it consumes the selections a preceding launches = 1 call left in the workspace;
+ * 3: both (== loki_decode).  Same arguments and workspace as loki_decode; LOKI_ERR_UNSUPPORTED for
+ * single-launch plans.  Not a serving entry point. */
+loki_status loki_decode_phase(const loki_decode_args* args, int32_t launches, void* stream);
+
 /* Scratch bytes loki_decode needs for `args` (0 for on-chip plans).
  * The workspace must be ZERO-FILLED before its first use (cudaMemset); every
  * launch leaves it zero-filled again (the persistent kernel's ticket counter,

@@ -188,6 +188,14 @@ class DecodeCall:
             _lib.check(self.lib.loki_decode(self._argp, stream if stream is not None else stream_of(self.device)))
         return self.outputs
 
+    def run_phase(self, launches: int, stream=None):
+        """Phase timing only (loki_decode_phase): 1 = the A launch (approx scores + top-k), 2 = the B launch
+        (exact attention over the selection A left in the workspace), 3 = both."""
+        with on_device(self.device):
+            _lib.check(self.lib.loki_decode_phase(self._argp, int(launches),
+                                                  stream if stream is not None else stream_of(self.device)))
+        return self.outputs
+
 
 def lens_tensor(lens, B, device):
     if isinstance(lens, torch.Tensor):

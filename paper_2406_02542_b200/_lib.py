@@ -41,7 +41,7 @@ SELECT_TOPK_SHARED = 4  # opt-in GQA: one selection per KV group on the summed g
 # every symbol include/loki_b200.h declares (checked by tests/test_host.py)
 EXPORTED = (
     "loki_last_error", "loki_abi_version", "loki_device_check", "loki_decode",
-    "loki_decode_workspace_bytes", "loki_decode_plan", "loki_append_kv",
+    "loki_decode_workspace_bytes", "loki_decode_plan", "loki_decode_phase", "loki_append_kv",
     "loki_gathered_scores", "loki_weighted_sum", "loki_weighted_sum_workspace",
     "loki_softmax_rows", "loki_rope", "loki_index_status", "loki_set_phase_trace", "loki_project_rows",
 )
@@ -76,6 +76,7 @@ _SIGS = {
     "loki_abi_version": (_I32, []),
     "loki_device_check": (_I32, [_I32]),
     "loki_decode": (_I32, [ctypes.POINTER(DecodeArgs), _P]),
+    "loki_decode_phase": (_I32, [ctypes.POINTER(DecodeArgs), _I32, _P]),
     "loki_decode_workspace_bytes": (_I32, [ctypes.POINTER(DecodeArgs), ctypes.POINTER(ctypes.c_size_t)]),
     "loki_decode_plan": (_I32, [ctypes.POINTER(DecodeArgs), ctypes.POINTER(_I32), ctypes.POINTER(_I32),
                                 ctypes.POINTER(ctypes.c_size_t)]),

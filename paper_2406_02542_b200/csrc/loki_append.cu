@@ -64,6 +64,9 @@ __global__ void __launch_bounds__(kThreads) append_kernel(
         "l"(Ph), "r"(bytes), "r"(smem_addr(&p_bar))
         : "memory");
   }
+  // every thread waits on p_bar below: none may touch it before thread 0 has initialised it
+  // (compute-sanitizer racecheck / synccheck, r02)
+  if (stage_p) __syncthreads();
   // PDL: inputs (the previous layer's products in a real model) are read below
   asm volatile("griddepcontrol.wait;" ::: "memory");
 

@@ -247,6 +247,7 @@ struct PipePlan {
   TmaGeom tg{};
   int G_T = 1;
   int G_Ta = 1;  // group size the A launch is instantiated for (1 for group-shared selection)
+  bool mode3 = false;  // the opt-in on-chip lists A launch (LOKI_LISTS)
   loki::PipeParams blay{};  // group-shared: the B-only launch's shared-memory layout (no histogram)
   size_t smem_b = 0;
   bool big = false;
@@ -269,8 +270,12 @@ bool pipe_eligible(const loki_decode_args* a) {
   const int G_T = loki::next_pow2(g.Hq / g.Hkv);
   const size_t e = g.dtype == LOKI_DTYPE_BF16 ? 2 : 4;
   const loki::RowSpace rs = loki::row_space(g);
+  // dense decode (SELECT_ALL) runs as a B-only launch over every row when no diagnostics are asked for
+  const bool dense = a->select_mode == LOKI_SELECT_ALL && g.dtype == LOKI_DTYPE_BF16 && a->idx_out == nullptr &&
+                     a->approx_out == nullptr && a->weights_out == nullptr && env_int("LOKI_PIPE_DENSE", 1) != 0;
   return env_int("LOKI_PIPE", 1) != 0 &&
-         (a->select_mode == LOKI_SELECT_TOPK || a->select_mode == LOKI_SELECT_TOPK_SHARED) && a->ext_scores == nullptr &&
+         (a->select_mode == LOKI_SELECT_TOPK || a->select_mode == LOKI_SELECT_TOPK_SHARED || dense) &&
+         a->ext_scores == nullptr &&
          a->out != nullptr && a->K != nullptr && a->V != nullptr && rs.ok && aligned(a->K, 16) &&
          aligned(a->V, 16) && (g.stride_s * e) % 16 == 0 &&
          a->S_max < (1 << 24) && loki::pipe_supported(g.dtype, g.D, G_T) && a->cluster_override == 0;
@@ -295,7 +300,12 @@ loki_status shared_unsupported(const loki_decode_args* a) {
   return s != LOKI_OK ? s : fail(LOKI_ERR_UNSUPPORTED, "group-shared selection: no pipe plan");
 }
 
-loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
+loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
+  // dense decode: B-only launch over every row; the (unused) lead-column geometry is planned for d = 32
+  const bool dense = a_in->select_mode == LOKI_SELECT_ALL;
+  loki_decode_args ad = *a_in;
+  if (dense) ad.d = a_in->g.D < 32 ? a_in->g.D : 32;
+  const loki_decode_args* a = &ad;
   const loki_kv_geom& g = a->g;
   const int G = g.Hq / g.Hkv;
   const int G_T = loki::next_pow2(G);
@@ -323,6 +333,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // head, so not with the 8192-row chunks
   // (r01: no gain on the tensor-core path at C2, 210.5 vs 211.3 us, and 16 KB more smem: opt-in there)
   p.shared = shared ? G : 0;
+  p.dense = dense ? 1 : 0;
   p.split_k = !shared && env_int("LOKI_SPLITK", mma ? 0 : 1) != 0 && d < g.D &&
               (mma ? (d == 32 && g.D == 128 && G_T <= 4) : (d % vec == 0 && ((g.D - d) * e) % 32 == 0));
   if (mma) p.r3 = 8;
@@ -346,6 +357,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // register arrays -- MHA-sized parts (a k-fraction of the rows is selected, whatever the group size)
   const bool shared_lists = shared && env_int("LOKI_GLOBAL_LISTS", 1) != 0;
   if (shared_lists) Lc = env_int("LOKI_LISTS_LC", a->S_max >= 16384 ? 8192 : 4096);
+  if (dense) Lc = env_int("LOKI_DENSE_LC", a->S_max >= 8192 ? 8192 : 4096);
   if (Lc % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", Lc, p.r1);
   p.Lc = Lc;
   p.nA = loki::ceil_div(a->S_max, Lc);
@@ -359,7 +371,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   p.spec = env_int("LOKI_SPEC", 0) != 0 && G_T <= 4 && a->idx_out == nullptr && p.La == p.Lc;  // opt-in (net loss)
   p.ccap = a->S_max / 4 > 2048 ? a->S_max / 4 : 2048;
   pl->smem = loki::pipe_layout(G_T, &p);
-  if (shared) {  // the B-only launch keeps no histogram: its own, smaller layout (room for the larger parts)
+  if (shared || dense) {  // the B-only launch keeps no histogram: its own, smaller layout (room for larger parts)
     pl->blay = p;
     pl->blay.hbits = 0;
     pl->smem_b = loki::pipe_layout(G_T, &pl->blay);
@@ -373,13 +385,14 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // r01: split layers beat the single launch on MHA bf16 (C2 212 -> 205 us, TGT 626 -> 603 us)
   // (short sequences keep one launch: S = 4K 125 vs 137 us split)
   // (r01: GQA too, C3 866 -> 742, C4 989 -> 875, C5s 4445 -> 3468 us)
-  pl->split = (shared || env_int("LOKI_PIPE_SPLIT", a->S_max >= 8192 ? 1 : 0) != 0) && g.dtype == LOKI_DTYPE_BF16 &&
-              !p.spec;
+  pl->split = (shared || dense || env_int("LOKI_PIPE_SPLIT", a->S_max >= 8192 ? 1 : 0) != 0) &&
+              g.dtype == LOKI_DTYPE_BF16 && !p.spec;
+  if (dense && !pl->split) return fail(LOKI_ERR_UNSUPPORTED, "pipe: dense decode needs the B-only launch");
   pl->G_Ta = shared ? 1 : G_T;  // group-shared: the A launch ranks once per unit (a G = 1 problem)
   if (pl->split) {  // the A-only launch needs no B-item entry region
     pl->smem1 = (size_t)p.off_ents + 1024;
     const int occ1 = loki::pipe_ctas_per_sm(g.dtype, g.D, pl->G_Ta, pl->smem1, pl->big, 1);
-    const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, shared ? pl->smem_b : pl->smem, pl->big, 2);
+    const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, (shared || dense) ? pl->smem_b : pl->smem, pl->big, 2);
     if (occ1 < 1 || occ2 < 1) pl->split = false;
     // A chunks of >= 8192 rows (r01: C2 197.9 -> 193.0 us); the A launch has no lag to feed.  Groups of 8:
     // >= 32768 rows (fewer arrivals into the serial 8-head selection; r01 C5s 3398 -> 3232 us,
@@ -422,7 +435,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   // group-shared selection always runs here: its selection is a G = 1 problem on the summed query (one lane
   // per lead row, so the G = 1 box rule applies), whatever the number of units
   const bool g1_lead = (p.lead_swz == 64 || p.lead_swz == 128) && p.r1 % (p.lead_swz == 64 ? 64 : 32) == 0;
-  if (pl->split && (G_T == 1 || shared) && !p.spec && !p.split_k && g1_lead &&
+  if (pl->split && !dense && (G_T == 1 || shared) && !p.spec && !p.split_k && g1_lead &&
       env_int("LOKI_SELECT_WS", 1) != 0 && units >= sm_count()) {
     // The warp-specialised A launch (one 16-warp CTA per SM, one whole unit per item): a stream group
     // streams unit i's lead columns while a select group selects unit i - 1, so the selection never
@@ -469,6 +482,7 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
     const int o1 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, s1, pl->big, 3);
     if (s1 <= kSmemMax && o1 >= 1) {
       p.lists = 1;
+      pl->mode3 = true;
       p.off_kchip = p.off_ents;
       pl->smem1 = s1;
       const int a_ctas = env_int("LOKI_PIPE_A_CTAS", o1);
@@ -515,7 +529,8 @@ loki_status make_pipe_plan(const loki_decode_args* a, PipePlan* pl) {
   return LOKI_OK;
 }
 
-loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
+// phases: bit 0 the A-only launch, bit 1 the B-only launch (split plans; both = the decode step).
+loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream, int phases = 3) {
   const loki_kv_geom& g = a->g;
   if (a->workspace == nullptr || a->workspace_bytes < pl.ws)
     return fail(LOKI_ERR_SHAPE, "workspace of %zu bytes required", pl.ws);
@@ -569,7 +584,8 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
   loki::TmaDesc maps[4];
   if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, p.mma != 0, p.lead_swz, maps))
     return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
-  cudaError_t e;
+  cudaError_t e = cudaSuccess;
+  if (!pl.split && phases != 3) return fail(LOKI_ERR_UNSUPPORTED, "single-launch plan: phases run together");
   if (pl.split) {
     loki::PipeParams pa = p, pb = p;
     pa.n_tickets = (long long)p.units * p.nAa;
@@ -585,7 +601,8 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
                       (pa.n_tickets + pb.n_tickets) * 4 <= (long long)loki::g_phase_trace_ctas * 8;
     pa.trace = fits ? loki::g_phase_trace : nullptr;
     pb.trace = fits ? loki::g_phase_trace + pa.n_tickets * 4 : nullptr;
-    if (pl.ws_select) {
+    if (!(phases & 1) || p.dense) {  // (dense decode: no A launch)
+    } else if (pl.ws_select) {
       pa.off_ring = pl.sel_layout.off_ring;
       pa.off_bars = pl.sel_layout.off_bars;
       pa.off_hist = pl.sel_layout.off_hist;
@@ -597,7 +614,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
                                    static_cast<cudaStream_t>(stream));
     } else {
       e = loki::launch_pipe(pa, g.dtype, pl.G_Ta, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big,
-                            p.lists ? 3 : 1);
+                            pl.mode3 ? 3 : 1);
     }
     size_t smem2 = pl.smem;
     if (pl.smem_b > 0) {
@@ -607,12 +624,12 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream) {
       pb.off_ents = pl.blay.off_ents;
       smem2 = pl.smem_b;
     }
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && (phases & 2))
       e = loki::launch_pipe(pb, g.dtype, pl.G_T, pl.grid2, smem2, maps, static_cast<cudaStream_t>(stream), pl.big, 2);
   } else {
     e = loki::launch_pipe(p, g.dtype, pl.G_T, pl.grid, pl.smem, maps, static_cast<cudaStream_t>(stream), pl.big);
   }
-  if (e == cudaSuccess && p.lists && a->weights_out != nullptr)  // diagnostics: weights from the entry lists
+  if (e == cudaSuccess && (phases & 2) && p.lists && a->weights_out != nullptr)  // diagnostics: weights from lists
     e = loki::launch_pipe_weights(p, static_cast<cudaStream_t>(stream));
   if (e == cudaSuccess) e = cudaGetLastError();
   return cuda_status(e, "loki_decode (pipe) launch");
@@ -681,6 +698,19 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
   if (rows_per_cta) *rows_per_cta = plan.Lmax;
   if (smem_bytes) *smem_bytes = plan.smem;
   return LOKI_OK;
+}
+
+loki_status loki_decode_phase(const loki_decode_args* a, int32_t launches, void* stream) {
+  loki_status s = validate(a);
+  if (s != LOKI_OK) return s;
+  loki_decode_args a1;
+  a = canonical_mode(a, &a1);
+  if (launches < 1 || launches > 3) return fail(LOKI_ERR_DOMAIN, "launches %d not in {1, 2, 3}", launches);
+  PipePlan pl;
+  if (!pipe_eligible(a)) return fail(LOKI_ERR_UNSUPPORTED, "phase launches exist on the pipe path only");
+  s = make_pipe_plan(a, &pl);
+  if (s != LOKI_OK) return s;
+  return run_pipe(a, pl, stream, launches);
 }
 
 loki_status loki_decode(const loki_decode_args* a, void* stream) {

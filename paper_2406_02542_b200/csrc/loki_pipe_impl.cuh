@@ -1621,7 +1621,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   const int pidx = half < 0 ? q : 2 * q + half;             // partial-state slot
   const int narrive = half < 0 ? nparts : 2 * nparts;     // B items of this unit
   uint32_t* cu = p.ctrl + 2 + 4 * (size_t)u;
-  if (tid == 0) {
+  if (tid == 0 && !p.dense) {
     // a unit's selection is published by a CTA that is already running, so the wait always ends; the
     // guard turns a broken invariant into an error instead of a hung GPU (p.spin_ns, 0 = no guard)
     unsigned spins = 0;
@@ -1645,7 +1645,11 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
   float* apx = reinterpret_cast<float*>(ents + p.Lc);  // [G][Lc] phase-1 partial logits, log2 domain
   // this part's selected rows, ascending, with head masks: one L2 round trip for the keys
   int n = 0;
-  if (nrows > 0 && p.lists) {  // the A item published this unit's ordered entries and their part offsets
+  if (p.dense) {  // dense decode (vanilla_attention): every row of the part, every head
+    const uint32_t full = ((1u << G) - 1u) << 24;
+    n = nrows;
+    for (int i = tid; i < n; i += kPT) ents[i] = full | (uint32_t)(row0 + i);
+  } else if (nrows > 0 && p.lists) {  // the A item published this unit's ordered entries and their part offsets
     const uint32_t* lo = p.loff + (size_t)u * (2 * p.nA + 1);
     const int h0 = half < 0 ? 2 * q : 2 * q + half;
     const int e0 = (int)__ldcg(&lo[h0]);
