@@ -254,6 +254,7 @@ struct PipePlan {
   bool split = false;  // A-only launch + B-only launch (MHA bf16)
   bool ws_select = false;  // the A launch is the warp-specialised pipe_select_kernel (layout in sel_layout)
   bool ws_onchip = false;  // ... with the keys on chip (lists mode)
+  int ws_groups = 1;       // ... its key arrays per unit (per-head GQA: the group size)
   loki::PipeParams sel_layout{};
   int grid = 0, grid1 = 0, grid2 = 0;
   size_t smem1 = 0;
@@ -356,7 +357,11 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   // then copy their slice instead of re-deriving it from the keys, so their size is free of the key-scan
   // register arrays -- MHA-sized parts (a k-fraction of the rows is selected, whatever the group size)
   const bool shared_lists = shared && env_int("LOKI_GLOBAL_LISTS", 1) != 0;
-  if (shared_lists) Lc = env_int("LOKI_LISTS_LC", a->S_max >= 16384 ? 8192 : 4096);
+  // per-head groups in split layers publish union lists too (head masks per entry)
+  const bool head_lists = !shared && !dense && G_T > 1 && g.dtype == LOKI_DTYPE_BF16 && a->S_max >= 8192 &&
+                          env_int("LOKI_PIPE_SPLIT", 1) != 0 && env_int("LOKI_HEAD_LISTS", 1) != 0;
+  const bool lists_plan = shared_lists || head_lists;
+  if (lists_plan) Lc = env_int("LOKI_LISTS_LC", a->S_max >= 16384 ? 8192 : 4096);
   if (dense) Lc = env_int("LOKI_DENSE_LC", a->S_max >= 8192 ? 8192 : 4096);
   if (Lc % p.r1 != 0) return fail(LOKI_ERR_UNSUPPORTED, "pipe: chunk %d vs box rows %d", Lc, p.r1);
   p.Lc = Lc;
@@ -371,7 +376,7 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   p.spec = env_int("LOKI_SPEC", 0) != 0 && G_T <= 4 && a->idx_out == nullptr && p.La == p.Lc;  // opt-in (net loss)
   p.ccap = a->S_max / 4 > 2048 ? a->S_max / 4 : 2048;
   pl->smem = loki::pipe_layout(G_T, &p);
-  if (shared || dense) {  // the B-only launch keeps no histogram: its own, smaller layout (room for larger parts)
+  if (shared || dense || head_lists) {  // the B-only launch keeps no histogram: its own, smaller layout
     pl->blay = p;
     pl->blay.hbits = 0;
     pl->smem_b = loki::pipe_layout(G_T, &pl->blay);
@@ -392,7 +397,7 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   if (pl->split) {  // the A-only launch needs no B-item entry region
     pl->smem1 = (size_t)p.off_ents + 1024;
     const int occ1 = loki::pipe_ctas_per_sm(g.dtype, g.D, pl->G_Ta, pl->smem1, pl->big, 1);
-    const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, (shared || dense) ? pl->smem_b : pl->smem, pl->big, 2);
+    const int occ2 = loki::pipe_ctas_per_sm(g.dtype, g.D, G_T, pl->smem_b > 0 ? pl->smem_b : pl->smem, pl->big, 2);
     if (occ1 < 1 || occ2 < 1) pl->split = false;
     // A chunks of >= 8192 rows (r01: C2 197.9 -> 193.0 us); the A launch has no lag to feed.  Groups of 8:
     // >= 32768 rows (fewer arrivals into the serial 8-head selection; r01 C5s 3398 -> 3232 us,
@@ -435,7 +440,11 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   // group-shared selection always runs here: its selection is a G = 1 problem on the summed query (one lane
   // per lead row, so the G = 1 box rule applies), whatever the number of units
   const bool g1_lead = (p.lead_swz == 64 || p.lead_swz == 128) && p.r1 % (p.lead_swz == 64 ? 64 : 32) == 0;
-  if (pl->split && !dense && (G_T == 1 || shared) && !p.spec && !p.split_k && g1_lead &&
+  // per-head groups (bf16, tensor-core lead path): the same launch with G key arrays in the workspace,
+  // the select group taking the heads in turn; B items re-derive the union from the keys
+  const bool gqa_ws = G_T > 1 && !shared && g.dtype == LOKI_DTYPE_BF16 && (p.lead_swz == 64 || p.lead_swz == 128) &&
+                      env_int("LOKI_SELECT_WS_GQA", 1) != 0;
+  if (pl->split && !dense && ((G_T == 1 || shared) ? g1_lead : gqa_ws) && !p.spec && !p.split_k &&
       env_int("LOKI_SELECT_WS", 1) != 0 && units >= sm_count()) {
     // The warp-specialised A launch (one 16-warp CTA per SM, one whole unit per item): a stream group
     // streams unit i's lead columns while a select group selects unit i - 1, so the selection never
@@ -447,21 +456,23 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
     // Entry lists need power-of-two half parts; diagnostic weights need the keys left in the workspace
     // (the merge re-derives each head's selection from them), so such calls keep the key path
     const bool pow2 = ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0;
-    const bool onchip = ps.La <= env_int("LOKI_ONCHIP_ROWS", 8192) && pow2;
+    const int GS = gqa_ws ? G_T : 1;  // key arrays / histograms per unit in the A launch
+    const bool onchip = GS == 1 && ps.La <= env_int("LOKI_ONCHIP_ROWS", 8192) && pow2;
     // ring stages per stream warp: 3 where they fit (r02: TGT 591 -> 566 us, C2 177 -> 174 us), else 2
     size_t sw = 0;
     int ow = 0;
     for (int nst = env_int("LOKI_SELECT_STAGES", 3); nst >= 2 && ow < 1; --nst) {
       ps.nst = nst;
-      sw = loki::pipe_select_layout(&ps, onchip);
-      ow = sw <= kSmemMax ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, onchip, sw) : 0;
+      sw = loki::pipe_select_layout(&ps, onchip, GS);
+      ow = sw <= kSmemMax ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, onchip, sw, GS) : 0;
     }
     if (ow >= 1) {
       p.La = ps.La;
       p.nAa = 1;
       // (units whose keys stay in the workspace publish lists too: the select group streams them back once
       // more and writes the entries in place, so B items copy slices instead of re-deriving them)
-      p.lists = (onchip || (pow2 && shared_lists)) ? 1 : 0;
+      p.lists = (onchip || (pow2 && lists_plan)) ? 1 : 0;
+      pl->ws_groups = GS;
       pl->ws_select = true;
       pl->ws_onchip = onchip;
       pl->sel_layout = ps;
@@ -471,8 +482,9 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   }
   if (shared && !g1_lead)  // (few units: the chunked A-only launch with G = 1 items, MODE 1)
     return fail(LOKI_ERR_UNSUPPORTED, "group-shared selection: lead rows of %d B in %d-row boxes", p.lead_swz, p.r1);
-  if (shared && !pl->ws_select && shared_lists && ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0)
+  if (pl->split && !pl->ws_select && lists_plan && ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0)
     p.lists = 1;  // the last A arriver's selection also emits the unit's entry list (select_unit)
+  if (lists_plan && !p.lists) return fail(LOKI_ERR_UNSUPPORTED, "pipe: list plan without a split layer");
   const size_t kchip = (size_t)G_T * p.La * 4;
   if (!pl->ws_select && pl->split && G_T == 1 && !pl->big && env_int("LOKI_LISTS", 0) != 0 && p.nAa == 1 &&
       !p.spec && !p.split_k && a->idx_out == nullptr && a->weights_out == nullptr &&
@@ -506,6 +518,7 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   off = loki::align_up(off + (size_t)units * G * HB * 4, 256);
   pl->off_keys = off;
   p.kstride = loki::ceil_div(g.S_cap, 4) * 4;
+  p.sel_stride = p.kstride * (shared ? 1 : G);  // entry lists overwrite a unit's (first) key array
   off = loki::align_up(off + (size_t)units * G * p.kstride * 4, 256);
   pl->off_tcs = off;
   off = loki::align_up(off + (size_t)units * G * 8, 256);
@@ -611,7 +624,7 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream, int 
       pa.cand_bytes = pl.sel_layout.cand_bytes;
       pa.nst = pl.sel_layout.nst;
       e = loki::launch_pipe_select(pa, g.dtype, pl.ws_onchip, pl.grid1, pl.smem1, maps,
-                                   static_cast<cudaStream_t>(stream));
+                                   static_cast<cudaStream_t>(stream), pl.ws_groups);
     } else {
       e = loki::launch_pipe(pa, g.dtype, pl.G_Ta, pl.grid1, pl.smem1, maps, static_cast<cudaStream_t>(stream), pl.big,
                             pl.mode3 ? 3 : 1);

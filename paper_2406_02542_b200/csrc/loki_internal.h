@@ -101,7 +101,8 @@ struct PipeParams {
   int off_kchip;
   int off_cand, cand_bytes;  // warp-specialised A launch: the select group's candidate buffers
   long long spin_ns;  // B items trap after waiting this long for their unit's selection (0: never)
-  uint32_t* sel;     // [units][kstride] (aliases keys: lists mode writes no global keys)
+  uint32_t* sel;     // [units][sel_stride] (aliases keys: entries are written in place over a unit's keys)
+  int sel_stride;    // words between units' entry lists: kstride x key arrays per unit in the A launch
   // group-shared selection (LOKI_SELECT_TOPK_SHARED): the query heads of a KV group share one selection,
   // made on the group's summed query (sum_g q_g[:d] . K[j, :d]); the A launch runs it as a G = 1 problem
   // (its params carry G = 1, shared = the group size), the B launch attends every head (full masks)
@@ -189,11 +190,11 @@ int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode 
 // warp-specialised A launch of split MHA bf16 layers (lead rows of 64 / 128 B), one unit per item: sets the
 // layout offsets in *p (ring, bars, double-buffered histograms, on-chip keys or the key stream's buffers,
 // candidates) and returns its bytes.  onchip: keys on chip + lists mode; else keys in the workspace
-size_t pipe_select_layout(PipeParams* p, bool onchip);
+size_t pipe_select_layout(PipeParams* p, bool onchip, int G_T = 1);
 cudaError_t launch_pipe_weights(const PipeParams& p, cudaStream_t st);
-int pipe_select_ctas_per_sm(int dtype, int lead_rb, bool onchip, size_t smem);
+int pipe_select_ctas_per_sm(int dtype, int lead_rb, bool onchip, size_t smem, int G_T = 1);
 cudaError_t launch_pipe_select(const PipeParams& p, int dtype, bool onchip, int grid, size_t smem,
-                               const TmaDesc* maps, cudaStream_t st);
+                               const TmaDesc* maps, cudaStream_t st, int G_T = 1);
 int pipe_warps();
 // 128-row blocks per warp in a B part (Lc = blocks * 128 * warps), shared by kernel and host
 __host__ __device__ constexpr int pipe_blocks_per_warp(int G_T, bool big) {

@@ -56,14 +56,14 @@ int pipe_ctas_per_sm(int dtype, int D, int G_T, size_t smem, bool big, int mode)
   return 0;
 }
 
-size_t pipe_select_layout(PipeParams* p, bool onchip) {
+size_t pipe_select_layout(PipeParams* p, bool onchip, int G_T) {
   size_t off = 0;
   p->off_ring = 0;
   off += (size_t)kPW * p->nst * p->stage_bytes;
   p->off_bars = (int)off;
   off = align_up(off + (size_t)(kPW * p->nst + 6) * 8, 16);
   p->off_hist = (int)off;
-  off = align_up(off + 2 * (size_t)(1u << p->hbits) * 4, 128);
+  off = align_up(off + 2 * (size_t)G_T * (1u << p->hbits) * 4, 128);  // [2][G_T][HB]
   p->off_kchip = (int)off;  // on-chip keys [2][La], or the key stream's two chunk buffers
   off = align_up(off + 2 * (size_t)(onchip ? p->La : kCK) * 4, 128);
   p->off_cand = (int)off;
@@ -72,29 +72,22 @@ size_t pipe_select_layout(PipeParams* p, bool onchip) {
   return off + 1024;  // slack for aligning the dynamic shared memory base to 1024 B
 }
 
-template <int RB, bool ONCHIP>
+template <int RB, bool ONCHIP, int G_T>
 KernelAttrs& select_attrs() {
   static KernelAttrs a;
   return a;
 }
 
-template <int RB, bool ONCHIP>
+template <int RB, bool ONCHIP, int G_T>
 static int select_occ(size_t smem) {
-  return select_attrs<RB, ONCHIP>().occupancy(
-      reinterpret_cast<const void*>(pipe_select_kernel<__nv_bfloat16, RB, ONCHIP>), 2 * kPT, smem);
+  return select_attrs<RB, ONCHIP, G_T>().occupancy(
+      reinterpret_cast<const void*>(pipe_select_kernel<__nv_bfloat16, RB, ONCHIP, G_T>), 2 * kPT, smem);
 }
 
-int pipe_select_ctas_per_sm(int dtype, int lead_rb, bool onchip, size_t smem) {
-  if (dtype != LOKI_DTYPE_BF16) return 0;
-  if (lead_rb == 64) return onchip ? select_occ<64, true>(smem) : select_occ<64, false>(smem);
-  if (lead_rb == 128) return onchip ? select_occ<128, true>(smem) : select_occ<128, false>(smem);
-  return 0;
-}
-
-template <int RB, bool ONCHIP>
+template <int RB, bool ONCHIP, int G_T>
 static cudaError_t launch_select_t(const PipeParams& p, int grid, size_t smem, const TmaDesc* maps, cudaStream_t st) {
-  auto kern = pipe_select_kernel<__nv_bfloat16, RB, ONCHIP>;
-  cudaError_t e = select_attrs<RB, ONCHIP>().ensure(reinterpret_cast<const void*>(kern), smem);
+  auto kern = pipe_select_kernel<__nv_bfloat16, RB, ONCHIP, G_T>;
+  cudaError_t e = select_attrs<RB, ONCHIP, G_T>().ensure(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -110,15 +103,46 @@ static cudaError_t launch_select_t(const PipeParams& p, int grid, size_t smem, c
   return cudaLaunchKernelEx(&cfg, kern, p, m[0]);
 }
 
+// Instantiations: G = 1 (MHA, group-shared) with on-chip or workspace keys; per-head groups of 2 / 4 / 8
+// with workspace keys.  op = 0: occupancy for `smem`; op = 1: launch.
+template <int RB>
+static int select_dispatch(int op, bool onchip, int G_T, const PipeParams* p, int grid, size_t smem,
+                           const TmaDesc* maps, cudaStream_t st, cudaError_t* err) {
+#define LOKI_SEL(ONC, G)                                                          \
+  {                                                                               \
+    if (op == 0) return select_occ<RB, ONC, G>(smem);                             \
+    *err = launch_select_t<RB, ONC, G>(*p, grid, smem, maps, st);                 \
+    return 0;                                                                     \
+  }
+  if (G_T == 1) {
+    if (onchip) LOKI_SEL(true, 1)
+    LOKI_SEL(false, 1)
+  }
+  if (!onchip) {
+    if (G_T == 2) LOKI_SEL(false, 2)
+    if (G_T == 4) LOKI_SEL(false, 4)
+    if (G_T == 8) LOKI_SEL(false, 8)
+  }
+#undef LOKI_SEL
+  *err = cudaErrorInvalidValue;
+  return 0;
+}
+
+int pipe_select_ctas_per_sm(int dtype, int lead_rb, bool onchip, size_t smem, int G_T) {
+  if (dtype != LOKI_DTYPE_BF16) return 0;
+  cudaError_t e = cudaSuccess;
+  if (lead_rb == 64) return select_dispatch<64>(0, onchip, G_T, nullptr, 0, smem, nullptr, nullptr, &e);
+  if (lead_rb == 128) return select_dispatch<128>(0, onchip, G_T, nullptr, 0, smem, nullptr, nullptr, &e);
+  return 0;
+}
+
 cudaError_t launch_pipe_select(const PipeParams& p, int dtype, bool onchip, int grid, size_t smem,
-                               const TmaDesc* maps, cudaStream_t st) {
+                               const TmaDesc* maps, cudaStream_t st, int G_T) {
   if (dtype != LOKI_DTYPE_BF16) return cudaErrorInvalidValue;
-  if (p.lead_swz == 64)
-    return onchip ? launch_select_t<64, true>(p, grid, smem, maps, st) : launch_select_t<64, false>(p, grid, smem, maps, st);
-  if (p.lead_swz == 128)
-    return onchip ? launch_select_t<128, true>(p, grid, smem, maps, st)
-                  : launch_select_t<128, false>(p, grid, smem, maps, st);
-  return cudaErrorInvalidValue;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (p.lead_swz == 64) select_dispatch<64>(1, onchip, G_T, &p, grid, smem, maps, st, &e);
+  else if (p.lead_swz == 128) select_dispatch<128>(1, onchip, G_T, &p, grid, smem, maps, st, &e);
+  return e;
 }
 
 cudaError_t launch_pipe_weights(const PipeParams& p, cudaStream_t st) {

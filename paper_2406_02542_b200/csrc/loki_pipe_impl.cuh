@@ -315,6 +315,9 @@ __device__ __forceinline__ void sel_stamp(const PipeParams& p, int u, int k) {
 template <typename Grp>
 __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned long long Tc, uint32_t* kbuf,
                                   uint64_t* sbar, unsigned& sphase, PipeShared& sh);
+template <typename Grp, int G_T>
+__device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint32_t* kbuf, uint64_t* sbar,
+                                        unsigned& sphase, PipeShared& sh);
 
 template <int G_T>
 __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, uint32_t* hist, uint64_t* sbar,
@@ -558,9 +561,12 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
     }
     __syncthreads();
   }
-  if (p.lists && G == 1) {  // lists mode (one selection per unit): ordered entries for the B items
+  if (p.lists) {  // lists mode: the unit's ordered entries for the B items
     __syncthreads();
-    emit_lists_global<CtaGroup>(p, u, S, __ldcg(&p.tcs[u]), reinterpret_cast<uint32_t*>(ring), sbar, sphase, sh);
+    if constexpr (G_T == 1)
+      emit_lists_global<CtaGroup>(p, u, S, __ldcg(&p.tcs[u]), reinterpret_cast<uint32_t*>(ring), sbar, sphase, sh);
+    else
+      emit_lists_global_heads<CtaGroup, G_T>(p, u, S, reinterpret_cast<uint32_t*>(ring), sbar, sphase, sh);
   }
   if (tid == 0) cu[0] = 0u;  // A arrivals: ready for the next launch
   sel_stamp(p, u, 5);
@@ -710,7 +716,7 @@ __device__ void emit_lists(const PipeParams& p, int u, int S, const uint32_t* ks
   const int lane = lane_id(), w = Grp::warp();
   const int G = p.G;
   const int lhs = 31 - __clz(p.Lc / 2);  // Lc / 2 is a power of two
-  uint32_t* dst = p.sel + (size_t)u * p.kstride;
+  uint32_t* dst = p.sel + (size_t)u * p.sel_stride;
   uint32_t* lo = p.loff + (size_t)u * (2 * p.nA + 1);
   unsigned long long Tc[G_T];
 #pragma unroll
@@ -1654,7 +1660,7 @@ __device__ int item_B(const PipeParams& p, const CUtensorMap* krow_map, const CU
     const int h0 = half < 0 ? 2 * q : 2 * q + half;
     const int e0 = (int)__ldcg(&lo[h0]);
     n = (int)__ldcg(&lo[h0 + (half < 0 ? 2 : 1)]) - e0;
-    const uint32_t* src = p.sel + (size_t)u * p.kstride + e0;
+    const uint32_t* src = p.sel + (size_t)u * p.sel_stride + e0;
     for (int i = tid; i < n; i += kPT) ents[i] = __ldcg(&src[i]);
   } else if (nrows > 0) {
     // group-shared selection: one key array and one threshold per unit; a selected row serves every head
@@ -2000,14 +2006,15 @@ struct KeyStreamG {
 // Same composite-key rule as select_unit / select_onchip; publishes tcs[u].
 template <typename Grp>
 __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, uint32_t* kbuf, uint64_t* sbar,
-                              unsigned& sphase, uint8_t* scratch, int scratch_bytes, PipeShared& sh) {
+                              unsigned& sphase, uint8_t* scratch, int scratch_bytes, PipeShared& sh, int g = 0) {
+  const size_t ug = (size_t)u * p.G + g;  // this (unit, head)'s keys and threshold (per-head GQA: G heads in turn)
   const int tid = Grp::tid(), lane = lane_id();
   const int hb = p.hbits, HB = 1 << hb;
   const int kb = k_of(p, S);
   const int cap = scratch_bytes / 16;
   unsigned long long* candA = reinterpret_cast<unsigned long long*>(scratch);
   unsigned long long* candB = candA + cap;
-  const uint32_t* keys = p.keys + (size_t)u * p.kstride;
+  const uint32_t* keys = p.keys + ug * p.kstride;
   const KeyStreamG<Grp> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S > 0 ? S : 1, kCK)};
   unsigned long long Tc;
   if (kb <= 0 || kb >= S) {
@@ -2139,17 +2146,18 @@ __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, ui
       });
     }
     Grp::sync();
-    if (tid == 0) {
-      const int gs = unit_heads(p);
+    if (tid == 0) {  // group-shared: the one selection's offsets serve every head of the group
+      const size_t r0 = p.shared > 1 ? (size_t)u * p.shared : ug;
+      const int nr = p.shared > 1 ? p.shared : 1;
       unsigned run = 0;
       for (int i = 0; i < nh; ++i) {
-        for (int g = 0; g < gs; ++g) p.poff[((size_t)u * gs + g) * nh + i] = run;
+        for (int r = 0; r < nr; ++r) p.poff[(r0 + r) * nh + i] = run;
         run += cnt[i];
       }
     }
     Grp::sync();
   }
-  if (tid == 0) p.tcs[u] = Tc;
+  if (tid == 0) p.tcs[ug] = Tc;
   Grp::sync();
 }
 
@@ -2165,7 +2173,7 @@ __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned lo
   constexpr int PER = kCK / Grp::kThreads;  // contiguous keys per thread and chunk
   const int tid = Grp::tid();
   const int lhs = 31 - __clz(p.Lc / 2);     // Lc / 2 is a power of two (>= PER)
-  uint32_t* keys = p.keys + (size_t)u * p.kstride;
+  uint32_t* keys = p.keys + (size_t)u * p.sel_stride;  // (== the unit's keys: one array per unit here)
   uint32_t* lo = p.loff + (size_t)u * (2 * p.nA + 1);
   const unsigned full = shared_mask(p) << 24;
   int32_t* idx_dst = nullptr;
@@ -2206,6 +2214,102 @@ __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned lo
   Grp::sync();
 }
 
+// Ordered emission for per-head groups (G_T > 1, keys in the workspace): the G key arrays of a unit stream
+// back together (chunks of kCK / G_T rows per head in one buffer), every row some head selected becomes
+// an entry (head mask << 24 | row), ascending, written in place over the unit's head-0 keys (same rule
+// as emit_lists_global: positions never pass their rows, the chunks in flight lie beyond), plus the half
+// parts' entry offsets and, for diagnostics, each head's own ascending index row.
+template <typename Grp, int G_T>
+__device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint32_t* kbuf, uint64_t* sbar,
+                                        unsigned& sphase, PipeShared& sh) {
+  constexpr int C = kCK / G_T;              // rows per chunk (one buffer holds G_T x C keys)
+  constexpr int PER = C / Grp::kThreads;    // contiguous rows per thread and chunk
+  static_assert(PER >= 1, "chunk too small");
+  const int tid = Grp::tid();
+  const int G = p.G;
+  const int lhs = 31 - __clz(p.Lc / 2);
+  uint32_t* dst = p.sel + (size_t)u * p.sel_stride;  // == the unit's head-0 keys
+  const uint32_t* keys = p.keys + (size_t)u * G * p.kstride;
+  uint32_t* lo = p.loff + (size_t)u * (2 * p.nA + 1);
+  unsigned long long Tc[G_T];
+#pragma unroll
+  for (int g = 0; g < G_T; ++g) Tc[g] = g < G ? __ldcg(&p.tcs[(size_t)u * G + g]) : ~0ull;
+  int32_t* idx0 = p.idx_out != nullptr
+                      ? p.idx_out + ((size_t)(u / p.Hkv) * p.Hq + (size_t)(u % p.Hkv) * G) * p.idx_stride
+                      : nullptr;
+  const int nchunk = ceil_div(S > 0 ? S : 1, C);
+  auto issue = [&](int c) {
+    if (tid == 0 && c < nchunk) {
+      const int base = c * C;
+      const int rows = min(C, p.kstride - base);
+      const unsigned bytes = (unsigned)(((rows * 4) + 15) & ~15);
+      uint64_t* bar = &sbar[c & 1];
+      mbar_expect_tx(bar, bytes * (unsigned)G);
+      for (int g = 0; g < G; ++g)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(kbuf + (c & 1) * kCK + g * C)),
+            "l"(keys + (size_t)g * p.kstride + base), "r"(bytes), "r"(smem_u32(bar))
+            : "memory");
+    }
+  };
+  unsigned base = 0, hbase[G_T];
+#pragma unroll
+  for (int g = 0; g < G_T; ++g) hbase[g] = 0u;
+  if (S > 0) {
+    if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // keys came from generic stores
+    issue(0);
+    issue(1);
+    for (int c = 0; c < nchunk; ++c) {
+      const int bi = c & 1;
+      mbar_wait(&sbar[bi], (sphase >> bi) & 1u);
+      sphase ^= 1u << bi;
+      const uint32_t* kc = kbuf + bi * kCK;
+      const int j0 = c * C, t0 = tid * PER;
+      const int nrow = min(C, S - j0);
+      unsigned m[PER];
+      unsigned cnt = 0;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) {
+        m[e] = 0u;
+        if (t0 + e < nrow)
+#pragma unroll
+          for (int g = 0; g < G_T; ++g)
+            if (g < G && comp_key(kc[g * C + t0 + e], j0 + t0 + e) >= Tc[g]) m[e] |= 1u << g;
+        cnt += m[e] != 0u;
+      }
+      unsigned tot;
+      unsigned at = base + block_incl_scan<Grp>(cnt, sh, &tot) - cnt;
+      const int r0 = j0 + t0;
+      if (t0 < nrow && (r0 & ((1 << lhs) - 1)) == 0) lo[r0 >> lhs] = at;
+      if (idx0 != nullptr) {  // diagnostics: each head's ascending rows at its own positions
+#pragma unroll
+        for (int g = 0; g < G_T; ++g) {
+          if (g >= G) break;
+          unsigned cg = 0;
+#pragma unroll
+          for (int e = 0; e < PER; ++e) cg += (m[e] >> g) & 1u;
+          unsigned tg;
+          unsigned pg = hbase[g] + block_incl_scan<Grp>(cg, sh, &tg) - cg;
+#pragma unroll
+          for (int e = 0; e < PER; ++e)
+            if ((m[e] >> g) & 1u) idx0[(size_t)g * p.idx_stride + pg++] = r0 + e;
+          hbase[g] += tg;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < PER; ++e)
+        if (m[e]) dst[at++] = (m[e] << 24) | (uint32_t)(r0 + e);
+      base += tot;
+      Grp::sync();  // the group is done with buffer bi (and its writes precede later chunks') before the refill
+      issue(c + 2);
+    }
+  }
+  if (tid == 0)
+    for (int q = S > 0 ? ((S + (1 << lhs) - 1) >> lhs) : 0; q <= 2 * p.nA; ++q) lo[q] = base;
+  Grp::sync();
+}
+
 // ------------------------------------------------------------------ warp-specialised A launch
 // Split layers whose units are one A chunk (lists mode, MHA): a 16-warp CTA per
 // SM runs phase 1 and the selection as a two-stage pipeline over units.
@@ -2225,9 +2329,12 @@ using SelectGrp = WarpGroup<kPW, kPW, 2>;
 // select group also emits the ordered entry lists (lists mode); else (long
 // sequences) the stream group writes the keys to the L2-resident workspace, the
 // select group streams them back (select_global) and publishes the threshold.
-template <typename T, int RB, bool ONCHIP>
+// G_T > 1 (per-head GQA, workspace keys): the stream group scores the G heads on the tensor cores
+// (lead_consume_mma) into G key arrays and G histograms; the select group selects the heads in turn.
+template <typename T, int RB, bool ONCHIP, int G_T = 1>
 __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParams p,
                                                                  const __grid_constant__ CUtensorMap lead_map) {
+  static_assert(G_T == 1 || !ONCHIP, "per-head groups keep their keys in the workspace");
   constexpr int E = sizeof(T);
   constexpr int Q2 = RB / (2 * E);
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -2242,7 +2349,7 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
   uint64_t* full = bars + (size_t)kPW * nsw;  // [2]
   uint64_t* empty = full + 2;                 // [2]
   uint64_t* sbar = empty + 2;                 // [2] the select group's key stream (!ONCHIP)
-  uint32_t* hist2 = reinterpret_cast<uint32_t*>(smem + p.off_hist);   // [2][HB]
+  uint32_t* hist2 = reinterpret_cast<uint32_t*>(smem + p.off_hist);   // [2][G_T][HB]
   uint32_t* kbuf2 = reinterpret_cast<uint32_t*>(smem + p.off_kchip);  // ONCHIP: [2][La]; else [2][kCK]
   uint8_t* cand = smem + p.off_cand;
   if (threadIdx.x == 0) {
@@ -2286,9 +2393,9 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       const int bb = u / p.Hkv, hk = u % p.Hkv;
       int S = p.lens[bb];
       S = S < 0 ? 0 : (S > p.S_max ? p.S_max : S);
-      uint32_t* hist = hist2 + (size_t)b * HB;
-      uint32_t* keys = ONCHIP ? kbuf2 + (size_t)b * p.La : p.keys + (size_t)u * p.kstride;
-      for (int j = tid; j < HB; j += kPT) hist[j] = 0u;
+      uint32_t* hist = hist2 + (size_t)b * G_T * HB;
+      uint32_t* keys = ONCHIP ? kbuf2 + (size_t)b * p.La : p.keys + (size_t)u * p.G * p.kstride;
+      for (int j = tid; j < G_T * HB; j += kPT) hist[j] = 0u;
       StreamGrp::sync();
       const int n = S < p.La ? S : p.La;
       if (n > 0) {
@@ -2304,8 +2411,39 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
           RingPos q = rp;
           for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
         }
-        const int gs = unit_heads(p);  // 1, or the group whose summed query ranks the rows (shared mode)
+        const int gs = unit_heads(p);  // 1, the group size, or the group whose summed query ranks (shared)
         const size_t qrow0 = (size_t)bb * p.Hq + (size_t)hk * gs;
+        if constexpr (G_T > 1) {  // per-head GQA: G heads on the tensor cores (q in three bf16 terms)
+          uint32_t qf[3][4][2];
+          const int g8 = lane >> 2, t4 = lane & 3;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            float v[4], r1v[4], r2v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int dim = 16 * ks + 2 * t4 + (i & 1) + (i >> 1) * 8;
+              v[i] = (g8 < p.G && dim < p.d) ? p.q_hat[(qrow0 + g8) * p.D + dim] : 0.f;
+              r1v[i] = v[i] - bf16_hi(v[i]);
+              r2v[i] = r1v[i] - bf16_hi(r1v[i]);
+            }
+            qf[0][ks][0] = pack_bf16(v[0], v[1]);
+            qf[0][ks][1] = pack_bf16(v[2], v[3]);
+            qf[1][ks][0] = pack_bf16(r1v[0], r1v[1]);
+            qf[1][ks][1] = pack_bf16(r1v[2], r1v[3]);
+            qf[2][ks][0] = pack_bf16(r2v[0], r2v[1]);
+            qf[2][ks][1] = pack_bf16(r2v[2], r2v[3]);
+          }
+          float* approx_u = p.approx_out ? p.approx_out + qrow0 * p.S_cap : nullptr;
+          for (int k = 0; k < mine; ++k, rp.advance(1)) {
+            mbar_wait(&wbar[rp.slot], rp.phase);
+            const int box = w + k * kPW;
+            const int rows_here = min(R1, n - box * R1);
+            lead_consume_mma<RB, G_T>(p, wring + rp.slot * SB, rows_here, qf, p.G, keys + box * R1, p.kstride,
+                                      nullptr, approx_u ? approx_u + box * R1 : nullptr, hist, HB, hshift);
+            __syncwarp();
+            if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+          }
+        } else {
         unsigned long long q2[Q2];
 #pragma unroll
         for (int j = 0; j < Q2; ++j) {  // (independent loads, all in flight together)
@@ -2333,6 +2471,7 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
           __syncwarp();
           if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
         }
+        }
       }
       StreamGrp::sync();  // every key and histogram count of this unit is in shared memory
       if (p.approx_out != nullptr && p.shared > 1) {  // diagnostics: each head of the group reports the group score
@@ -2358,7 +2497,13 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       const uint32_t* keys = kbuf2 + (size_t)b * p.La;
       const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
       sel_stamp<SelectGrp>(p, u, 0);
-      if constexpr (ONCHIP) {
+      if constexpr (G_T > 1) {  // per-head GQA: the G heads in turn, thresholds for the B items' key path
+        for (int g = 0; g < p.G; ++g)
+          select_global<SelectGrp>(p, u, S, hist2 + ((size_t)b * G_T + g) * HB, kbuf2, sbar, sphase, cand,
+                                   p.cand_bytes, sh, g);
+        sel_stamp<SelectGrp>(p, u, 4);
+        if (p.lists) emit_lists_global_heads<SelectGrp, G_T>(p, u, S, kbuf2, sbar, sphase, sh);
+      } else if constexpr (ONCHIP) {
         select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
         sel_stamp<SelectGrp>(p, u, 4);
         emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
@@ -2387,18 +2532,36 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
   }
 }
 
-// LokiDiagnostics.weights of a lists-mode launch (one selection per unit: G = 1 or group-shared): entry i
-// of unit u is row sel[u][i] for every head, weight exp2(logit - M) / L with the head's merged (M, L).
-// Diagnostics only: a separate small launch keeps this code out of the B items' register budget.
+// LokiDiagnostics.weights of a lists-mode launch: head g's weights follow its own ascending rows -- the
+// entries whose mask has bit g -- weight exp2(logit - M) / L with the head's merged (M, L).  Diagnostics
+// only: a separate small launch keeps this code out of the B items' register budget.
 __global__ void __launch_bounds__(256) pipe_weights_kernel(const PipeParams p) {
+  __shared__ unsigned wsum[8];
   const int u = blockIdx.x, g = blockIdx.y;
-  const uint32_t* sel = p.sel + (size_t)u * p.kstride;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t* sel = p.sel + (size_t)u * p.sel_stride;
   const int total = (int)p.loff[(size_t)u * (2 * p.nA + 1) + 2 * p.nA];
   const float M = p.ml[((size_t)u * p.G + g) * 2], invL = 1.f / p.ml[((size_t)u * p.G + g) * 2 + 1];
   const float* lg = p.logits + ((size_t)u * p.G + g) * p.S_cap;
   const size_t qrow = (size_t)(u / p.Hkv) * p.Hq + (size_t)(u % p.Hkv) * p.G + g;
   float* dst = p.weights_out + qrow * p.idx_stride;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) dst[i] = exp2f(lg[sel[i] & 0xFFFFFFu] - M) * invL;
+  unsigned base = 0;
+  for (int i0 = 0; i0 < total; i0 += 256) {
+    const int i = i0 + threadIdx.x;
+    const uint32_t e = i < total ? sel[i] : 0u;
+    const bool on = i < total && ((e >> (24 + g)) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    unsigned before = 0, tot = 0;
+    for (int k = 0; k < 8; ++k) {
+      before += k < w ? wsum[k] : 0u;
+      tot += wsum[k];
+    }
+    if (on) dst[base + before + __popc(bal & ((1u << lane) - 1u))] = exp2f(lg[e & 0xFFFFFFu] - M) * invL;
+    base += tot;
+    __syncthreads();
+  }
 }
 
 }  // namespace
