@@ -14,9 +14,16 @@ namespace loki {
 namespace {
 
 constexpr int kBatch = 2;
-constexpr int kThreads = 128;
+constexpr int kThreads = 512;  // r02: 128 -> 512 threads, the matvec split over row blocks (C2 K0 12.7 us alone)
 constexpr int kVecChunk = 8;
 constexpr int kSmemPMaxD = 128;  // P [D][D] fp32 staged on chip up to D = 128 (64 KB)
+
+// Row blocks of the K0 matvec: the largest power of two KS with KS * D <= kThreads that divides D.
+__host__ __device__ constexpr int row_blocks(int D) {
+  int ks = 1;
+  while (2 * ks * D <= kThreads && D % (2 * ks) == 0) ks *= 2;
+  return ks;
+}
 
 // rope.py:47-55: out[:h] = lo*cos - hi*sin ; out[h:] = lo*sin + hi*cos (fp64)
 __device__ __forceinline__ void rope_pair(double lo, double hi, double theta, double& olo, double& ohi) {
@@ -106,13 +113,19 @@ __global__ void __launch_bounds__(kThreads) append_kernel(
   }
   __syncthreads();
 
-  // y = x @ P (fp32 accumulate in index order, like the reference's float32 matmul);
-  // four vectors per pass, four inputs per step: float4 broadcast reads of x
-  for (int col = threadIdx.x; col < D; col += kThreads) {
+  // y = x @ P: thread (col, kq) accumulates rows [kq R, (kq + 1) R) of P for column col (fp32, index
+  // order), the KS partial sums are then added in kq order; four vectors per pass, float4 broadcast reads
+  // of x.  (KS = kThreads / D row blocks: the dependent FMA chain is D / KS long instead of D.)
+  const int KS = row_blocks(D);
+  const int R = D / KS;
+  float* part = y + (size_t)nv4 * D;  // [KS][nv4][D]
+  for (int t = threadIdx.x; t < KS * D; t += kThreads) {
+    const int col = t % D, kq = t / D;
+    const int i_lo = kq * R, i_hi = i_lo + R;
     for (int v0 = 0; v0 < nv4; v0 += 4) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-      if (Ph && (D & 3)) {  // odd widths: plain scalar walk
-        for (int i = 0; i < D; ++i) {
+      if (Ph && ((D & 3) || (R & 3))) {  // odd widths: plain scalar walk
+        for (int i = i_lo; i < i_hi; ++i) {
           const float pij = P_SMEM ? Ps[i * D + col] : __ldg(Ph + (size_t)i * D + col);
           a0 = fmaf(x[(v0 + 0) * D + i], pij, a0);
           a1 = fmaf(x[(v0 + 1) * D + i], pij, a1);
@@ -121,10 +134,11 @@ __global__ void __launch_bounds__(kThreads) append_kernel(
         }
       } else if (Ph) {
 #pragma unroll 4
-        for (int i = 0; i < D; i += 4) {
+        for (int i = i_lo; i < i_hi; i += 4) {
           float p4[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) p4[t] = P_SMEM ? Ps[(i + t) * D + col] : __ldg(Ph + (size_t)(i + t) * D + col);
+          for (int t4 = 0; t4 < 4; ++t4)
+            p4[t4] = P_SMEM ? Ps[(i + t4) * D + col] : __ldg(Ph + (size_t)(i + t4) * D + col);
           const float4 x0 = *reinterpret_cast<const float4*>(x + (v0 + 0) * D + i);
           const float4 x1 = *reinterpret_cast<const float4*>(x + (v0 + 1) * D + i);
           const float4 x2 = *reinterpret_cast<const float4*>(x + (v0 + 2) * D + i);
@@ -134,17 +148,24 @@ __global__ void __launch_bounds__(kThreads) append_kernel(
           a2 = fmaf(x2.w, p4[3], fmaf(x2.z, p4[2], fmaf(x2.y, p4[1], fmaf(x2.x, p4[0], a2))));
           a3 = fmaf(x3.w, p4[3], fmaf(x3.z, p4[2], fmaf(x3.y, p4[1], fmaf(x3.x, p4[0], a3))));
         }
-      } else {
+      } else if (kq == 0) {
         a0 = x[(v0 + 0) * D + col];
         a1 = x[(v0 + 1) * D + col];
         a2 = x[(v0 + 2) * D + col];
         a3 = x[(v0 + 3) * D + col];
       }
-      y[(v0 + 0) * D + col] = a0;
-      y[(v0 + 1) * D + col] = a1;
-      y[(v0 + 2) * D + col] = a2;
-      y[(v0 + 3) * D + col] = a3;
+      float* pp = part + ((size_t)kq * nv4 + v0) * D + col;
+      pp[0] = a0;
+      pp[D] = a1;
+      pp[2 * D] = a2;
+      pp[3 * D] = a3;
     }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv4 * D; i += kThreads) {  // partial sums in row-block order
+    float acc = part[i];
+    for (int kq = 1; kq < KS; ++kq) acc += part[(size_t)kq * nv4 * D + i];
+    y[i] = acc;
   }
   __syncthreads();
 
@@ -214,7 +235,8 @@ cudaError_t launch_append(const float* q_raw, const float* k_raw, const float* v
   const bool p_smem = P != nullptr && g.D <= kSmemPMaxD && (reinterpret_cast<uintptr_t>(P) % 16) == 0 &&
                       (P_head_stride % 4) == 0;
   const size_t nv4 = ((size_t)kBatch * per_b + 3) & ~(size_t)3;
-  const size_t smem = (size_t)2 * nv4 * g.D * sizeof(float) + (p_smem ? (size_t)g.D * g.D * sizeof(float) : 0);
+  const size_t ks = (size_t)row_blocks(g.D);  // row blocks of the matvec (partial sums on chip)
+  const size_t smem = (size_t)(2 + ks) * nv4 * g.D * sizeof(float) + (p_smem ? (size_t)g.D * g.D * sizeof(float) : 0);
   dim3 grid((unsigned)g.Hkv, (unsigned)ceil_div(g.B, kBatch));
   cudaError_t e;
   if (g.dtype == LOKI_DTYPE_BF16)

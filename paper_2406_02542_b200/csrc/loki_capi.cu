@@ -46,6 +46,7 @@ bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) %
 constexpr int kThreads = 256;
 constexpr size_t kSmemPreferred = 100 * 1024;
 constexpr size_t kSmemMax = 200 * 1024;
+constexpr size_t kSmemSelMax = 227 * 1024;  // the warp-specialised A launch: one CTA per SM, the whole SM's smem
 
 int k_for(const loki_decode_args* a, int S) {
   if (a->select_mode == LOKI_SELECT_ALL) return S;
@@ -464,7 +465,7 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
     for (int nst = env_int("LOKI_SELECT_STAGES", 3); nst >= 2 && ow < 1; --nst) {
       ps.nst = nst;
       sw = loki::pipe_select_layout(&ps, onchip, GS);
-      ow = sw <= kSmemMax ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, onchip, sw, GS) : 0;
+      ow = sw <= kSmemSelMax ? loki::pipe_select_ctas_per_sm(g.dtype, p.lead_swz, onchip, sw, GS) : 0;
     }
     if (ow >= 1) {
       p.La = ps.La;

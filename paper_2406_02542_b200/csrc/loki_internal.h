@@ -54,6 +54,10 @@ struct FusedParams {
 // B(u, *) tickets come `lag` units after A(u, *), so other CTAs keep HBM busy
 // while a unit's selection runs.  The workspace must be zero on first use;
 // every launch leaves it zero again (counters / histograms self-reset).
+// Key-stream buffers of the warp-specialised A launch's select group (16 KB each): the key passes are
+// L2-latency bound, so four chunks are kept in flight (r02: two left a 32K-key pass at ~7 GB/s).
+constexpr int kSelNB = 4;
+
 struct PipeParams {
   const float* q_hat;  // [B, Hq, D]
   int B, Hq, Hkv, G, D, S_cap;

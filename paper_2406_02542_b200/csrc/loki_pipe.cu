@@ -61,11 +61,11 @@ size_t pipe_select_layout(PipeParams* p, bool onchip, int G_T) {
   p->off_ring = 0;
   off += (size_t)kPW * p->nst * p->stage_bytes;
   p->off_bars = (int)off;
-  off = align_up(off + (size_t)(kPW * p->nst + 6) * 8, 16);
+  off = align_up(off + (size_t)(kPW * p->nst + 4 + kSelNB) * 8, 16);
   p->off_hist = (int)off;
   off = align_up(off + 2 * (size_t)G_T * (1u << p->hbits) * 4, 128);  // [2][G_T][HB]
-  p->off_kchip = (int)off;  // on-chip keys [2][La], or the key stream's two chunk buffers
-  off = align_up(off + 2 * (size_t)(onchip ? p->La : kCK) * 4, 128);
+  p->off_kchip = (int)off;  // on-chip keys [2][La], or the key stream's chunk buffers [kSelNB][kCK]
+  off = align_up(off + (onchip ? 2 * (size_t)p->La : (size_t)kSelNB * kCK) * 4, 128);
   p->off_cand = (int)off;
   p->cand_bytes = (onchip ? 16 : 32) * 1024;  // boundary-bin candidates, two buffers; more -> histogram levels
   off += (size_t)p->cand_bytes;

@@ -312,10 +312,10 @@ __device__ __forceinline__ void sel_stamp(const PipeParams& p, int u, int k) {
 // once <= 256 remain) and publishes tcs[u][g].  With idx_out it also
 // publishes each part's output offset (rows above the boundary per part +
 // candidates kept).
-template <typename Grp>
+template <typename Grp, int NB = 2>
 __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned long long Tc, uint32_t* kbuf,
                                   uint64_t* sbar, unsigned& sphase, PipeShared& sh);
-template <typename Grp, int G_T>
+template <typename Grp, int G_T, int NB = 2>
 __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint32_t* kbuf, uint64_t* sbar,
                                         unsigned& sphase, PipeShared& sh);
 
@@ -1960,12 +1960,12 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
 // Keys of one unit streamed from L2 through two shared buffers of kCK keys
 // (cp.async.bulk, the next chunk in flight while this one is scanned), run by a
 // thread group.  `sbar` are the group's two mbarriers, `sphase` their parities.
-template <typename Grp>
+template <typename Grp, int NB = 2>
 struct KeyStreamG {
   const uint32_t* src;
   int S, kstride;
-  uint32_t* buf;  // [2][kCK]
-  uint64_t* sbar;
+  uint32_t* buf;  // [NB][kCK]
+  uint64_t* sbar;  // [NB]
   unsigned* sphase;
   int nchunk;
   __device__ void issue(int c) const {
@@ -1973,29 +1973,36 @@ struct KeyStreamG {
       const int base = c * kCK;
       const int rows = min(kCK, kstride - base);
       const unsigned bytes = (unsigned)(((rows * 4) + 15) & ~15);
-      uint64_t* bar = &sbar[c & 1];
+      uint64_t* bar = &sbar[c % NB];
       mbar_expect_tx(bar, bytes);
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(buf + (c & 1) * kCK)),
+              smem_u32(buf + (c % NB) * kCK)),
           "l"(src + base), "r"(bytes), "r"(smem_u32(bar))
           : "memory");
     }
   }
   __device__ void start() const {
     if (Grp::tid() == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // keys came from generic stores
-    issue(0);
-    issue(1);
+    for (int c = 0; c < NB; ++c) issue(c);
+  }
+  // the chunks start() put in flight but run() never consumed (an early exit): wait them out
+  __device__ void drain() const {
+    for (int c = 0; c < NB && c < nchunk; ++c) {
+      mbar_wait(&sbar[c], (*sphase >> c) & 1u);
+      *sphase ^= 1u << c;
+    }
+    Grp::sync();
   }
   template <typename F>
   __device__ void run(F&& f) const {
     for (int c = 0; c < nchunk; ++c) {
-      const int bi = c & 1;
+      const int bi = c % NB;
       mbar_wait(&sbar[bi], (*sphase >> bi) & 1u);
       *sphase ^= 1u << bi;
       f(c * kCK, buf + bi * kCK, min(kCK, S - c * kCK));
       Grp::sync();  // the whole group is done with buffer bi before it is refilled
-      issue(c + 2);
+      issue(c + NB);
     }
   }
 };
@@ -2004,7 +2011,7 @@ struct KeyStreamG {
 // whose keys are in the L2-resident workspace (too many rows to keep on chip):
 // the select group of the warp-specialised A launch, for long MHA sequences.
 // Same composite-key rule as select_unit / select_onchip; publishes tcs[u].
-template <typename Grp>
+template <typename Grp, int NB = 2>
 __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, uint32_t* kbuf, uint64_t* sbar,
                               unsigned& sphase, uint8_t* scratch, int scratch_bytes, PipeShared& sh, int g = 0) {
   const size_t ug = (size_t)u * p.G + g;  // this (unit, head)'s keys and threshold (per-head GQA: G heads in turn)
@@ -2015,7 +2022,7 @@ __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, ui
   unsigned long long* candA = reinterpret_cast<unsigned long long*>(scratch);
   unsigned long long* candB = candA + cap;
   const uint32_t* keys = p.keys + ug * p.kstride;
-  const KeyStreamG<Grp> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S > 0 ? S : 1, kCK)};
+  const KeyStreamG<Grp, NB> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S > 0 ? S : 1, kCK)};
   unsigned long long Tc;
   if (kb <= 0 || kb >= S) {
     Tc = kb <= 0 ? ~0ull : 0ull;
@@ -2078,13 +2085,7 @@ __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, ui
       need -= sh.fb_above;
       cnt = sh.fb_cnt;
     }
-    if (started) {  // the prefetched chunks were never consumed: drain them before the buffers are reused
-      for (int c = 0; c < 2 && c < ks.nchunk; ++c) {
-        mbar_wait(&sbar[c], (sphase >> c) & 1u);
-        sphase ^= 1u << c;
-      }
-      Grp::sync();
-    }
+    if (started) ks.drain();  // the prefetched chunks were never consumed: drain them before the buffers are reused
     sel_stamp<Grp>(p, u, 2);
     Tc = nb >= 64 ? P : (P << (64 - nb));
     if (listed && cnt != need) {
@@ -2167,7 +2168,7 @@ __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, ui
 // exceeds its row, and rows are consumed chunk by chunk ahead of the writes; the chunks in flight lie
 // past every position written), plus each half part's entry offset in p.loff[u] and, for diagnostics,
 // the heads' ascending index rows.  One selection per unit: G = 1, or group-shared (every head's mask).
-template <typename Grp>
+template <typename Grp, int NB>
 __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned long long Tc, uint32_t* kbuf,
                                   uint64_t* sbar, unsigned& sphase, PipeShared& sh) {
   constexpr int PER = kCK / Grp::kThreads;  // contiguous keys per thread and chunk
@@ -2184,7 +2185,7 @@ __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned lo
   }
   unsigned base = 0;
   if (S > 0) {
-    const KeyStreamG<Grp> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
+    const KeyStreamG<Grp, NB> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S, kCK)};
     ks.start();
     ks.run([&](int j0, const uint32_t* kc, int nrow) {
       const int t0 = tid * PER;
@@ -2219,7 +2220,7 @@ __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned lo
 // an entry (head mask << 24 | row), ascending, written in place over the unit's head-0 keys (same rule
 // as emit_lists_global: positions never pass their rows, the chunks in flight lie beyond), plus the half
 // parts' entry offsets and, for diagnostics, each head's own ascending index row.
-template <typename Grp, int G_T>
+template <typename Grp, int G_T, int NB>
 __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint32_t* kbuf, uint64_t* sbar,
                                         unsigned& sphase, PipeShared& sh) {
   constexpr int C = kCK / G_T;              // rows per chunk (one buffer holds G_T x C keys)
@@ -2243,12 +2244,12 @@ __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint3
       const int base = c * C;
       const int rows = min(C, p.kstride - base);
       const unsigned bytes = (unsigned)(((rows * 4) + 15) & ~15);
-      uint64_t* bar = &sbar[c & 1];
+      uint64_t* bar = &sbar[c % NB];
       mbar_expect_tx(bar, bytes * (unsigned)G);
       for (int g = 0; g < G; ++g)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(kbuf + (c & 1) * kCK + g * C)),
+                smem_u32(kbuf + (c % NB) * kCK + g * C)),
             "l"(keys + (size_t)g * p.kstride + base), "r"(bytes), "r"(smem_u32(bar))
             : "memory");
     }
@@ -2258,10 +2259,9 @@ __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint3
   for (int g = 0; g < G_T; ++g) hbase[g] = 0u;
   if (S > 0) {
     if (tid == 0) asm volatile("fence.proxy.async.global;" ::: "memory");  // keys came from generic stores
-    issue(0);
-    issue(1);
+    for (int c = 0; c < NB; ++c) issue(c);
     for (int c = 0; c < nchunk; ++c) {
-      const int bi = c & 1;
+      const int bi = c % NB;
       mbar_wait(&sbar[bi], (sphase >> bi) & 1u);
       sphase ^= 1u << bi;
       const uint32_t* kc = kbuf + bi * kCK;
@@ -2302,7 +2302,7 @@ __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint3
         if (m[e]) dst[at++] = (m[e] << 24) | (uint32_t)(r0 + e);
       base += tot;
       Grp::sync();  // the group is done with buffer bi (and its writes precede later chunks') before the refill
-      issue(c + 2);
+      issue(c + NB);
     }
   }
   if (tid == 0)
@@ -2348,17 +2348,17 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bars);
   uint64_t* full = bars + (size_t)kPW * nsw;  // [2]
   uint64_t* empty = full + 2;                 // [2]
-  uint64_t* sbar = empty + 2;                 // [2] the select group's key stream (!ONCHIP)
+  uint64_t* sbar = empty + 2;                 // [kSelNB] the select group's key stream (!ONCHIP)
   uint32_t* hist2 = reinterpret_cast<uint32_t*>(smem + p.off_hist);   // [2][G_T][HB]
-  uint32_t* kbuf2 = reinterpret_cast<uint32_t*>(smem + p.off_kchip);  // ONCHIP: [2][La]; else [2][kCK]
+  uint32_t* kbuf2 = reinterpret_cast<uint32_t*>(smem + p.off_kchip);  // ONCHIP: [2][La]; else [kSelNB][kCK]
   uint8_t* cand = smem + p.off_cand;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kPW * nsw; ++i) mbar_init(&bars[i], 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], 1);
-      mbar_init(&sbar[b], 1);
     }
+    for (int b = 0; b < kSelNB; ++b) mbar_init(&sbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_desc(&lead_map);
   }
@@ -2499,18 +2499,19 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       sel_stamp<SelectGrp>(p, u, 0);
       if constexpr (G_T > 1) {  // per-head GQA: the G heads in turn, thresholds for the B items' key path
         for (int g = 0; g < p.G; ++g)
-          select_global<SelectGrp>(p, u, S, hist2 + ((size_t)b * G_T + g) * HB, kbuf2, sbar, sphase, cand,
-                                   p.cand_bytes, sh, g);
+          select_global<SelectGrp, kSelNB>(p, u, S, hist2 + ((size_t)b * G_T + g) * HB, kbuf2, sbar, sphase, cand,
+                                           p.cand_bytes, sh, g);
         sel_stamp<SelectGrp>(p, u, 4);
-        if (p.lists) emit_lists_global_heads<SelectGrp, G_T>(p, u, S, kbuf2, sbar, sphase, sh);
+        if (p.lists) emit_lists_global_heads<SelectGrp, G_T, kSelNB>(p, u, S, kbuf2, sbar, sphase, sh);
       } else if constexpr (ONCHIP) {
         select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
         sel_stamp<SelectGrp>(p, u, 4);
         emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
       } else {
-        select_global<SelectGrp>(p, u, S, hist2 + (size_t)b * HB, kbuf2, sbar, sphase, cand, p.cand_bytes, sh);
+        select_global<SelectGrp, kSelNB>(p, u, S, hist2 + (size_t)b * HB, kbuf2, sbar, sphase, cand, p.cand_bytes,
+                                         sh);
         sel_stamp<SelectGrp>(p, u, 4);
-        if (p.lists) emit_lists_global<SelectGrp>(p, u, S, p.tcs[u], kbuf2, sbar, sphase, sh);
+        if (p.lists) emit_lists_global<SelectGrp, kSelNB>(p, u, S, p.tcs[u], kbuf2, sbar, sphase, sh);
       }
       sel_stamp<SelectGrp>(p, u, 5);
       if (tid == 0) {
