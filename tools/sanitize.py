@@ -2,10 +2,11 @@
 
     compute-sanitizer --tool racecheck python tools/sanitize.py [--case all|split|single|gqa]
 
-Covers the persistent pipe kernel's three plans -- one launch (S < 8192), the
-split A-only + B-only pair (S >= 8192, PDL-chained, ready flags), a GQA group --
-with and without diagnostics, plus K0 (append) and the dense cluster kernel, at
-sizes the instrumented run finishes in minutes.  Not part of the product.
+Covers the persistent pipe kernel's plans -- one launch (S < 8192), the split
+A-only + B-only pair (S >= 8192, PDL-chained, ready flags), a GQA group, the
+group-shared selection (entry lists, the weights finalize launch) -- with and
+without diagnostics, plus K0 (append) and the dense B-only launch, at sizes the
+instrumented run finishes in minutes.  Not part of the product.
 """
 
 import argparse
@@ -27,6 +28,7 @@ CASES = {  # B, Hq, Hkv, S
     "single": (2, 2, 2, 4096),
     "split": (1, 2, 2, 8192),
     "gqa": (1, 8, 2, 8192),
+    "shared": (2, 8, 2, 9000),  # group-shared selection (chunked A launch + entry lists)
 }
 for name, (B, Hq, Hkv, S) in CASES.items():
     if a.case not in ("all", name):
@@ -34,8 +36,9 @@ for name, (B, Hq, Hkv, S) in CASES.items():
     K = torch.randn(B, Hkv, S, 128, device=dev, generator=gen).to(torch.bfloat16)
     V = torch.randn(B, Hkv, S, 128, device=dev, generator=gen).to(torch.bfloat16)
     q = torch.randn(B, Hq, 128, device=dev, generator=gen)
-    y = L.loki_decode(q, K, V, None, d=32, k_f=0.25)
-    y2, diag = L.loki_decode(q, K, V, None, d=32, k_f=0.25, diagnostics=True)
+    gs = "shared" if name == "shared" else "per_head"
+    y = L.loki_decode(q, K, V, None, d=32, k_f=0.25, group_select=gs)
+    y2, diag = L.loki_decode(q, K, V, None, d=32, k_f=0.25, diagnostics=True, group_select=gs)
     torch.cuda.synchronize()
     assert torch.equal(y, y2), name
     rows = torch.full((B,), S - 1, dtype=torch.int32, device=dev)
@@ -47,7 +50,7 @@ for name, (B, Hq, Hkv, S) in CASES.items():
                         positions=torch.full((B,), S - 1, dtype=torch.int64, device=dev))
     dec.step()
     dec.step()
-    if a.case in ("all", "single"):
-        L.dense_decode(q, K, V)
+    if name in ("single", "gqa"):
+        L.dense_decode(q, K, V)  # bf16: the B-only dense launch
     torch.cuda.synchronize()
     print(f"sanitize case {name}: ok (plan {dec.call.plan()})", flush=True)
