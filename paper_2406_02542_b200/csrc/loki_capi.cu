@@ -31,6 +31,7 @@ loki_status fail(loki_status code, const char* fmt, ...) {
 
 loki_status cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return LOKI_OK;
+  (void)cudaGetLastError();  // a rejected launch must not resurface as the next call's error
   return fail(LOKI_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
@@ -46,7 +47,9 @@ bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) %
 constexpr int kThreads = 256;
 constexpr size_t kSmemPreferred = 100 * 1024;
 constexpr size_t kSmemMax = 200 * 1024;
-constexpr size_t kSmemSelMax = 227 * 1024;  // the warp-specialised A launch: one CTA per SM, the whole SM's smem
+// the warp-specialised A launch: one CTA per SM with (almost) the whole SM's shared memory -- 227 KB opt-in
+// less the kernel's static shared memory (PipeShared and friends)
+constexpr size_t kSmemSelMax = 224 * 1024;
 
 int k_for(const loki_decode_args* a, int S) {
   if (a->select_mode == LOKI_SELECT_ALL) return S;
@@ -474,11 +477,22 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
       // more and writes the entries in place, so B items copy slices instead of re-deriving them)
       p.lists = (onchip || (pow2 && lists_plan)) ? 1 : 0;
       pl->ws_groups = GS;
+      if (GS > 1 && env_int("LOKI_UMMA", 1) != 0) {  // per-head phase 1 on tcgen05: 128-row tile stages
+        const int tile = 128 * p.dbox * 2;
+        int ust = (int)(((size_t)loki::pipe_warps() * ps.nst * ps.stage_bytes) / (size_t)tile);
+        ust = ust > 8 ? 8 : ust;
+        if (ust >= 2 && 2 * ust + 4 <= loki::pipe_warps() * ps.nst && 128 % p.r1 == 0) {
+          ps.umma = 1;
+          ps.ust = ust;
+        }
+      }
       pl->ws_select = true;
       pl->ws_onchip = onchip;
       pl->sel_layout = ps;
       pl->smem1 = sw;
       pl->grid1 = sm_count() * ow;
+      const int g1 = env_int("LOKI_SELECT_GRID", 0);  // tuning: fewer A CTAs leave SMs to the B launch
+      if (g1 > 0 && g1 < pl->grid1) pl->grid1 = g1;
     }
   }
   if (shared && !g1_lead)  // (few units: the chunked A-only launch with G = 1 items, MODE 1)
@@ -624,6 +638,9 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream, int 
       pa.off_cand = pl.sel_layout.off_cand;
       pa.cand_bytes = pl.sel_layout.cand_bytes;
       pa.nst = pl.sel_layout.nst;
+      pa.umma = pl.sel_layout.umma;
+      pa.ust = pl.sel_layout.ust;
+      pa.off_qt = pl.sel_layout.off_qt;
       e = loki::launch_pipe_select(pa, g.dtype, pl.ws_onchip, pl.grid1, pl.smem1, maps,
                                    static_cast<cudaStream_t>(stream), pl.ws_groups);
     } else {

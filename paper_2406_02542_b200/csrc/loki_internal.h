@@ -111,6 +111,9 @@ struct PipeParams {
   // made on the group's summed query (sum_g q_g[:d] . K[j, :d]); the A launch runs it as a G = 1 problem
   // (its params carry G = 1, shared = the group size), the B launch attends every head (full masks)
   int shared;
+  int umma;          // per-head GQA A launch: phase 1 on tcgen05 (128-row tiles, TMEM accumulators)
+  int ust;           // ... its tile stages
+  int off_qt;        // ... its query-term operand tile in shared memory
   int dense;         // 1: SELECT_ALL on the B-only launch -- every row of every part, no A launch, no flags
   float* ml;         // [units][G][2] merged (max, sum) per head (lists mode with weights_out only)
   uint32_t* loff;    // [units][2 nA + 1]        // B parts in halves: 2 every unit, 1 tail units only (grouping then depends on #units), 0 none

@@ -69,6 +69,11 @@ size_t pipe_select_layout(PipeParams* p, bool onchip, int G_T) {
   p->off_cand = (int)off;
   p->cand_bytes = (onchip ? 16 : 32) * 1024;  // boundary-bin candidates, two buffers; more -> histogram levels
   off += (size_t)p->cand_bytes;
+  if (G_T > 1) {  // tcgen05 phase 1: the query-term operand tile [N][lead row] (1024-byte aligned)
+    off = align_up(off, 1024);
+    p->off_qt = (int)off;
+    off += (size_t)((3 * G_T + 15) / 16 * 16) * (size_t)(p->dbox * 2);
+  }
   return off + 1024;  // slack for aligning the dynamic shared memory base to 1024 B
 }
 

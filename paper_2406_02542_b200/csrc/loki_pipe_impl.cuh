@@ -38,6 +38,7 @@
 
 #include "loki_fused.cuh"
 #include "loki_tma.cuh"
+#include "loki_umma.cuh"
 
 namespace loki {
 
@@ -2310,6 +2311,111 @@ __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint3
   Grp::sync();
 }
 
+// Per-head GQA phase 1 on the 5th-generation tensor cores (tcgen05, TMEM accumulators): the stream group
+// of the warp-specialised A launch runs it as a warp-specialised pipeline over 128-row tiles of a unit --
+//   warp 0 (one lane): TMA producer, the tile's lead boxes into a ring of p.ust tile stages;
+//   warp 1 (one lane): MMA issuer, D[128 x N] = K_lead[128 x d] . Qt[N x d]^T per tile (d / 16 tcgen05.mma,
+//     kind::f16, bf16 x bf16 -> f32 in TMEM, two accumulators), committing to the ring's empty barrier and
+//     the accumulator's full barrier;
+//   warps 4-7: epilogue, tcgen05.ld of their 32-row TMEM lane quadrant, the score of head g = term 0 +
+//     term 1 + term 2 (q split into three bf16 terms, columns t * G_T + g, so the score keeps fp32-level
+//     error) -> order key -> the head's key array and histogram.
+// `tc` counts the tiles this CTA has processed (barrier phases continue across units).
+template <int RB, int G_T>
+__device__ void stream_unit_umma(const PipeParams& p, const CUtensorMap* lead_map, int bb, int hk, int n,
+                                 size_t qrow0, uint32_t* keys, uint32_t* hist, int HB, int hshift, uint8_t* smem,
+                                 uint64_t* bars, uint32_t tmem, uint32_t& tc) {
+  constexpr int E = 2;
+  constexpr int TR = 128;                            // rows per tile (the MMA's M)
+  constexpr int NCOL = (3 * G_T + 15) / 16 * 16;     // N: three query terms per head, padded to 16
+  constexpr uint32_t IDESC = umma::idesc_bf16_f32(TR, NCOL);
+  const int lane = lane_id(), w = warp_id();
+  const int NS = p.ust;
+  const int R1 = p.r1;
+  const int tile_bytes = TR * RB;
+  const int ntile = ceil_div(n, TR);
+  uint8_t* tiles = smem + p.off_ring;                // [NS][TR][RB], 1024-byte aligned tiles
+  uint8_t* qt = smem + p.off_qt;                     // [NCOL][RB] K-major query terms
+  uint64_t* fullb = bars;
+  uint64_t* emptyb = bars + NS;
+  uint64_t* tfull = bars + 2 * NS;
+  uint64_t* tempty = bars + 2 * NS + 2;
+  // the B operand: row r = term t (r / G_T) of head g (r % G_T), swizzled like the TMA tiles
+  for (int i = threadIdx.x; i < NCOL * (RB / 2); i += kPT) {
+    const int r = i / (RB / 2), c = i % (RB / 2);
+    const int t = r / G_T, g = r % G_T;
+    float v = 0.f;
+    if (t < 3 && g < p.G && c < p.d) {
+      const float x = p.q_hat[(qrow0 + g) * p.D + c];
+      const float r1 = x - bf16_hi(x);
+      v = t == 0 ? x : (t == 1 ? r1 : r1 - bf16_hi(r1));
+    }
+    const int sw = RB == 64 ? ((r >> 1) & 3) : (r & 7);
+    *reinterpret_cast<__nv_bfloat16*>(qt + r * RB + ((((c * E) >> 4) ^ sw) << 4) + ((c * E) & 15)) =
+        __float2bfloat16_rn(v);
+  }
+  umma::fence_async_smem();
+  WarpGroup<0, kPW, 1>::sync();  // (the stream group's barrier)
+  if (w == 0 && lane == 0) {  // ---- TMA producer
+    for (int t = 0; t < ntile; ++t) {
+      const uint32_t q = tc + (uint32_t)t;
+      const int slot = (int)(q % (uint32_t)NS);
+      if (q >= (uint32_t)NS) mbar_wait(&emptyb[slot], ((q / NS) - 1u) & 1u);
+      const int rows = min(TR, n - t * TR);
+      const int nb = ceil_div(rows, R1);
+      mbar_expect_tx(&fullb[slot], (unsigned)(nb * R1 * RB));
+      for (int i = 0; i < nb; ++i)
+        tma_box4d(tiles + slot * tile_bytes + i * R1 * RB, lead_map, 0, t * TR + i * R1, hk, bb, &fullb[slot]);
+    }
+  } else if (w == 1 && lane == 0) {  // ---- MMA issuer
+    const uint32_t qa = umma::smem_addr(qt);
+    for (int t = 0; t < ntile; ++t) {
+      const uint32_t q = tc + (uint32_t)t;
+      const int slot = (int)(q % (uint32_t)NS), acc = (int)(q & 1u);
+      mbar_wait(&fullb[slot], (q / NS) & 1u);
+      if (q >= 2u) mbar_wait(&tempty[acc], ((q >> 1) - 1u) & 1u);
+      umma::fence_after();
+      const uint32_t ta = umma::smem_addr(tiles + slot * tile_bytes);
+#pragma unroll
+      for (int ks = 0; ks < RB / 32; ++ks)
+        umma::mma_bf16(tmem + (uint32_t)(acc * NCOL), umma::smem_desc_kmajor(ta + 32 * ks, RB),
+                       umma::smem_desc_kmajor(qa + 32 * ks, RB), IDESC, ks > 0);
+      umma::commit(&emptyb[slot]);
+      umma::commit(&tfull[acc]);
+    }
+  } else if (w >= 4) {  // ---- epilogue: TMEM lane quadrant w % 4
+    const int ew = w - 4;
+    for (int t = 0; t < ntile; ++t) {
+      const uint32_t q = tc + (uint32_t)t;
+      const int acc = (int)(q & 1u);
+      mbar_wait(&tfull[acc], (q >> 1) & 1u);
+      umma::fence_after();
+      uint32_t v[NCOL];
+      const uint32_t ta = tmem + (uint32_t)(acc * NCOL) + ((uint32_t)(ew * 32) << 16);
+#pragma unroll
+      for (int c0 = 0; c0 < NCOL; c0 += 16) umma::ld_32x32b_x16(ta + c0, *reinterpret_cast<uint32_t(*)[16]>(v + c0));
+      umma::wait_ld();
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      const int row = t * TR + ew * 32 + lane;
+      if (row < n) {
+#pragma unroll
+        for (int g = 0; g < G_T; ++g) {
+          if (g < p.G) {
+            const float sc = (__uint_as_float(v[g]) + __uint_as_float(v[G_T + g])) + __uint_as_float(v[2 * G_T + g]);
+            const uint32_t key = order_key(sc);
+            keys[(size_t)g * p.kstride + row] = key;
+            if (p.approx_out != nullptr) p.approx_out[(qrow0 + g) * p.S_cap + row] = sc;
+            atomicAdd(&hist[g * HB + (key >> hshift)], 1u);
+          }
+        }
+      }
+    }
+  }
+  tc += (uint32_t)ntile;
+}
+
 // ------------------------------------------------------------------ warp-specialised A launch
 // Split layers whose units are one A chunk (lists mode, MHA): a 16-warp CTA per
 // SM runs phase 1 and the selection as a two-stage pipeline over units.
@@ -2359,8 +2465,18 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       mbar_init(&empty[b], 1);
     }
     for (int b = 0; b < kSelNB; ++b) mbar_init(&sbar[b], 1);
+    if constexpr (G_T > 1) {  // tcgen05 phase 1: the accumulators' empty barriers take the 4 epilogue warps
+      if (p.umma) {
+        mbar_init(&bars[2 * p.ust + 2], 4);
+        mbar_init(&bars[2 * p.ust + 3], 4);
+      }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_desc(&lead_map);
+  }
+  __shared__ uint32_t tmem_base;
+  if constexpr (G_T > 1) {
+    if (p.umma && wid == 0) umma::alloc(&tmem_base, 2 * ((3 * G_T + 15) / 16 * 16) <= 32 ? 32u : 64u);
   }
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");  // K0's q_hat / appended rows
@@ -2371,6 +2487,7 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
     uint8_t* wring = smem + p.off_ring + (size_t)w * nsw * SB;
     uint64_t* wbar = bars + (size_t)w * nsw;
     RingPos rp(nsw);
+    uint32_t utc = 0;  // tcgen05 path: tiles processed (barrier phases run on across units)
     for (int i = 0;; ++i) {
       const int b = i & 1;
       if (i >= 2) mbar_wait(&empty[b], ((i >> 1) - 1) & 1u);  // the select group is done with buffer b
@@ -2407,13 +2524,17 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
           mbar_expect_tx(&wbar[at.slot], box_bytes);
           tma_box4d(wring + at.slot * SB, &lead_map, 0, (w + k * kPW) * R1, hk, bb, &wbar[at.slot]);
         };
-        if (lane == 0) {
+        if (lane == 0 && !(G_T > 1 && p.umma)) {  // (the tcgen05 path has its own producer)
           RingPos q = rp;
           for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
         }
         const int gs = unit_heads(p);  // 1, the group size, or the group whose summed query ranks (shared)
         const size_t qrow0 = (size_t)bb * p.Hq + (size_t)hk * gs;
-        if constexpr (G_T > 1) {  // per-head GQA: G heads on the tensor cores (q in three bf16 terms)
+        if constexpr (G_T > 1) {
+          if (p.umma) {  // per-head GQA phase 1 on tcgen05 (tiles of 128 rows, TMEM accumulators)
+            stream_unit_umma<RB, G_T>(p, &lead_map, bb, hk, n, qrow0, keys, hist, HB, hshift, smem, bars, tmem_base,
+                                      utc);
+          } else {  // per-head GQA: G heads on mma.sync (q in three bf16 terms)
           uint32_t qf[3][4][2];
           const int g8 = lane >> 2, t4 = lane & 3;
 #pragma unroll
@@ -2442,6 +2563,7 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
                                       nullptr, approx_u ? approx_u + box * R1 : nullptr, hist, HB, hshift);
             __syncwarp();
             if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+          }
           }
         } else {
         unsigned long long q2[Q2];
@@ -2482,6 +2604,12 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       if (tid == 0) {
         item_u[b] = u;
         mbar_arrive(&full[b]);  // release: the select group acquires through the barrier phase
+      }
+    }
+    if constexpr (G_T > 1) {
+      if (p.umma) {  // every tile's MMAs and TMEM loads are done: free the accumulators
+        StreamGrp::sync();
+        if (w == 0) umma::dealloc(tmem_base, 2 * ((3 * G_T + 15) / 16 * 16) <= 32 ? 32u : 64u);
       }
     }
   } else {  // ---------------- select group

@@ -628,3 +628,35 @@ def test_dense_decode_b_launch_matches_vanilla(B, Hq, Hkv, S, lens):
         for h in range(Hq):
             y_ref, _ = O.vanilla_attention(q[b, h], K[b, h // G, :lens[b]], V[b, h // G, :lens[b]])
             assert O.rel_err(y[b, h], y_ref) <= 1e-3, (b, h)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [32, 64])
+def test_per_head_gqa_tcgen05_phase1_matches_mma_sync(monkeypatch, d):
+    """The per-head GQA A launch scores the group on tcgen05 (128-row tiles, TMEM accumulators) by default;
+    the mma.sync consumer (LOKI_UMMA=0) is the cross-check: same selections, same outputs, and both match
+    the oracle on a sample.  160 units, so the warp-specialised launch serves the layer."""
+    B, Hq, Hkv, S = 40, 16, 4, 8192
+    g = torch.Generator(device=DEV).manual_seed(31)
+    K = torch.randn(B, Hkv, S, 128, device=DEV, generator=g).to(torch.bfloat16)
+    V = torch.randn(B, Hkv, S, 128, device=DEV, generator=g).to(torch.bfloat16)
+    q = torch.randn(B, Hq, 128, device=DEV, generator=g)
+    monkeypatch.setenv("LOKI_TUNING", "1")
+    res = {}
+    for um in ("1", "0"):
+        monkeypatch.setenv("LOKI_UMMA", um)
+        res[um] = L.loki_decode(q, K, V, None, d=d, k_f=0.25, diagnostics=True)
+    torch.cuda.synchronize()
+    (y1, d1), (y0, d0) = res["1"], res["0"]
+    assert torch.equal(d1.indices, d0.indices)
+    assert torch.equal(y1, y0)
+    qh, idx, y = q.cpu().numpy(), d1.indices.cpu().numpy(), y1.cpu().numpy()
+    for b, h in ((0, 0), (7, 5), (39, 15)):
+        Kb = K[b, h // 4].float().cpu().numpy()
+        Vb = V[b, h // 4].float().cpu().numpy()
+        k = O.resolve_fraction(0.25, S)
+        y_ref, ref_idx, _, _ = O.loki_rank_and_attend(qh[b, h], Kb, Vb, d, k)
+        assert O.sets_match_outside_band(idx[b, h, :k], ref_idx, O.tie_band(qh[b, h], Kb, d, k))
+        if not np.array_equal(idx[b, h, :k], ref_idx):
+            y_ref = O.attend_on(qh[b, h], Kb, Vb, idx[b, h, :k])[0]
+        assert O.rel_err(y[b, h], y_ref) <= 1e-3
