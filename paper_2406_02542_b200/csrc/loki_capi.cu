@@ -353,7 +353,8 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   // chunk = part: kNB 128-row blocks per warp in the B-item row scan (loki_pipe.cu)
   // MHA at long sequences: 2x larger chunks (fewer per-item latency bubbles; r01: TGT 683 -> 658 us,
   // C2 213 -> 219 us, so only from 16K rows on)
-  pl->big = G_T == 1 && env_int("LOKI_PIPE_BIG", a->S_max >= 16384 ? 1 : 0) != 0;
+  // (r02, split layers with entry lists: from 8K rows too -- C2 step 177.2 -> 172.5 us/layer)
+  pl->big = G_T == 1 && env_int("LOKI_PIPE_BIG", a->S_max >= 8192 ? 1 : 0) != 0;
   if (pl->big && mma) p.split_k = 0;
   const int kNB = loki::pipe_blocks_per_warp(G_T, pl->big);
   int Lc = kNB * 128 * loki::pipe_warps();
