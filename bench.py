@@ -43,8 +43,9 @@ METRIC = "Loki decode-attn µs/layer & speedup vs full attn; achieved HBM GB/s"
 
 CONFIGS = {
     # name: layers, B, Hq, Hkv, D, S, k_f, d_f, rope base, description
-    "C1": dict(layers=1, B=1, Hq=32, Hkv=32, D=128, S=4096, k_f=0.25, d_f=0.25, base=10000.0,
-               desc="single Llama2-7B-shaped layer, B=1, S=4096"),
+    # C1 is one layer's shape; 4 layers are stepped so the 67 MB per layer does not stay in the 126 MB L2
+    "C1": dict(layers=4, B=1, Hq=32, Hkv=32, D=128, S=4096, k_f=0.25, d_f=0.25, base=10000.0,
+               desc="Llama2-7B-shaped layer, B=1, S=4096 (4 layers stepped: L2-cold)"),
     "C2": dict(layers=32, B=16, Hq=32, Hkv=32, D=128, S=8192, k_f=0.25, d_f=0.25, base=10000.0,
                desc="Llama2-7B-shaped 32-layer decode attention, B=16, S=8192, pre-rotary PCA"),
     "C3": dict(layers=4, B=32, Hq=32, Hkv=8, D=128, S=32768, k_f=0.125, d_f=0.5, base=500000.0,

@@ -297,6 +297,22 @@ const loki_decode_args* canonical_mode(const loki_decode_args* a, loki_decode_ar
   return tmp;
 }
 
+// Small batches (B <= 4, MHA, bf16, up to 32K rows): one thread-block cluster of C CTAs per unit (phase 1 in
+// lockstep, DSMEM radix select, gather, DSMEM merge) beats the persistent pipe, whose per-unit selection is
+// serial -- r02 sweep (tools/one_layer.py): B = 1, S = 4K 35.8 -> 24.1 us (C = 8); B = 1, S = 32K 148 -> 70;
+// B = 2, S = 8K 108 -> 42 (C = 4); B = 4, S = 8K 131 -> 79 (C = 4); B = 8 breaks even.  C depends on B
+// only, so KV-head shards of a layer run the same per-unit plan (bit-identical).
+const loki_decode_args* small_batch_plan(const loki_decode_args* a, loki_decode_args* tmp) {
+  const loki_kv_geom& g = a->g;
+  if (a->select_mode != LOKI_SELECT_TOPK || a->cluster_override != 0 || g.Hq != g.Hkv ||
+      g.dtype != LOKI_DTYPE_BF16 || g.B > 4 || a->S_max > 32768 || a->ext_scores != nullptr ||
+      env_int("LOKI_SMALL_CLUSTER", 1) == 0)
+    return a;
+  *tmp = *a;
+  tmp->cluster_override = g.B == 1 ? 8 : 4;
+  return tmp;
+}
+
 loki_status shared_unsupported(const loki_decode_args* a) {
   if (!pipe_eligible(a))
     return fail(LOKI_ERR_UNSUPPORTED, "group-shared selection needs a TMA-addressable cache (16 B aligned rows)");
@@ -688,8 +704,8 @@ loki_status loki_device_check(int32_t device) {
 loki_status loki_decode_workspace_bytes(const loki_decode_args* a, size_t* bytes) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
-  loki_decode_args a1;
-  a = canonical_mode(a, &a1);
+  loki_decode_args a1, a2;
+  a = small_batch_plan(canonical_mode(a, &a1), &a2);
   {
     PipePlan pl;
     if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {
@@ -711,8 +727,8 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
                              size_t* smem_bytes) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
-  loki_decode_args a1;
-  a = canonical_mode(a, &a1);
+  loki_decode_args a1, a2;
+  a = small_batch_plan(canonical_mode(a, &a1), &a2);
   PipePlan pl;
   if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {  // persistent grid: 0 (-2: split, two launches)
     if (ctas_per_unit) *ctas_per_unit = pl.split ? -2 : 0;
@@ -735,8 +751,8 @@ loki_status loki_decode_plan(const loki_decode_args* a, int32_t* ctas_per_unit, 
 loki_status loki_decode_phase(const loki_decode_args* a, int32_t launches, void* stream) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
-  loki_decode_args a1;
-  a = canonical_mode(a, &a1);
+  loki_decode_args a1, a2;
+  a = small_batch_plan(canonical_mode(a, &a1), &a2);
   if (launches < 1 || launches > 3) return fail(LOKI_ERR_DOMAIN, "launches %d not in {1, 2, 3}", launches);
   PipePlan pl;
   if (!pipe_eligible(a)) return fail(LOKI_ERR_UNSUPPORTED, "phase launches exist on the pipe path only");
@@ -748,8 +764,8 @@ loki_status loki_decode_phase(const loki_decode_args* a, int32_t launches, void*
 loki_status loki_decode(const loki_decode_args* a, void* stream) {
   loki_status s = validate(a);
   if (s != LOKI_OK) return s;
-  loki_decode_args a1;
-  a = canonical_mode(a, &a1);
+  loki_decode_args a1, a2;
+  a = small_batch_plan(canonical_mode(a, &a1), &a2);
   {
     PipePlan pl;
     if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) return run_pipe(a, pl, stream);

@@ -220,7 +220,11 @@ CASES = [  # B, Hq, Hkv, D, S, k_f, d_f, dtype
 
 
 @pytest.mark.parametrize("case", CASES)
-def test_batched_decode_vs_oracle(case):
+@pytest.mark.parametrize("planner", ["auto", "pipe"])
+def test_batched_decode_vs_oracle(case, planner, monkeypatch):
+    if planner == "pipe":
+        monkeypatch.setenv("LOKI_TUNING", "1")
+        monkeypatch.setenv("LOKI_SMALL_CLUSTER", "0")
     B, Hq, Hkv, D, S, k_f, d_f, dt = case
     bf = dt == "bf16"
     q, K, V = make_batch(B, Hq, Hkv, D, S, seed=B * 1000 + S, bf16=bf)
@@ -525,7 +529,11 @@ PIPE_GEOMETRY = [  # D, Hq, Hkv, dtype, d: every consumer variant of the pipe ke
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("geom", PIPE_GEOMETRY, ids=lambda g: "D%d_Hq%d_Hkv%d_%s_d%d" % g)
-def test_pipe_geometry_matrix(geom):
+@pytest.mark.parametrize("planner", ["auto", "pipe"])
+def test_pipe_geometry_matrix(geom, planner, monkeypatch):
+    if planner == "pipe":  # small MHA batches default to the cluster kernel: keep the pipe kernel covered too
+        monkeypatch.setenv("LOKI_TUNING", "1")
+        monkeypatch.setenv("LOKI_SMALL_CLUSTER", "0")
     D, Hq, Hkv, dt, d = geom
     bf = dt == "bf16"
     S_cap = 9000
