@@ -316,7 +316,7 @@ __device__ __forceinline__ void sel_stamp(const PipeParams& p, int u, int k) {
 template <typename Grp, int NB = 2>
 __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned long long Tc, uint32_t* kbuf,
                                   uint64_t* sbar, unsigned& sphase, PipeShared& sh);
-template <typename Grp, int G_T, int NB = 2>
+template <typename Grp, int G_T, int NB = 2, int CKE = kCK>
 __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint32_t* kbuf, uint64_t* sbar,
                                         unsigned& sphase, PipeShared& sh);
 
@@ -567,7 +567,8 @@ __device__ void select_unit(const PipeParams& p, int u, int S, uint8_t* ring, ui
     if constexpr (G_T == 1)
       emit_lists_global<CtaGroup>(p, u, S, __ldcg(&p.tcs[u]), reinterpret_cast<uint32_t*>(ring), sbar, sphase, sh);
     else
-      emit_lists_global_heads<CtaGroup, G_T>(p, u, S, reinterpret_cast<uint32_t*>(ring), sbar, sphase, sh);
+      emit_lists_global_heads<CtaGroup, G_T, 2, (G_T * 1024 > kCK ? G_T * 1024 : kCK)>(  // (the whole ring)
+          p, u, S, reinterpret_cast<uint32_t*>(ring), sbar, sphase, sh);
   }
   if (tid == 0) cu[0] = 0u;  // A arrivals: ready for the next launch
   sel_stamp(p, u, 5);
@@ -1961,24 +1962,24 @@ __global__ void __launch_bounds__(kPT, MODE == 1 ? 3 : 2) pipe_decode_kernel(con
 // Keys of one unit streamed from L2 through two shared buffers of kCK keys
 // (cp.async.bulk, the next chunk in flight while this one is scanned), run by a
 // thread group.  `sbar` are the group's two mbarriers, `sphase` their parities.
-template <typename Grp, int NB = 2>
+template <typename Grp, int NB = 2, int CK = kCK>
 struct KeyStreamG {
   const uint32_t* src;
   int S, kstride;
-  uint32_t* buf;  // [NB][kCK]
+  uint32_t* buf;  // [NB][CK]
   uint64_t* sbar;  // [NB]
   unsigned* sphase;
   int nchunk;
   __device__ void issue(int c) const {
     if (Grp::tid() == 0 && c < nchunk) {
-      const int base = c * kCK;
-      const int rows = min(kCK, kstride - base);
+      const int base = c * CK;
+      const int rows = min(CK, kstride - base);
       const unsigned bytes = (unsigned)(((rows * 4) + 15) & ~15);
       uint64_t* bar = &sbar[c % NB];
       mbar_expect_tx(bar, bytes);
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(buf + (c % NB) * kCK)),
+              smem_u32(buf + (c % NB) * CK)),
           "l"(src + base), "r"(bytes), "r"(smem_u32(bar))
           : "memory");
     }
@@ -2001,7 +2002,7 @@ struct KeyStreamG {
       const int bi = c % NB;
       mbar_wait(&sbar[bi], (*sphase >> bi) & 1u);
       *sphase ^= 1u << bi;
-      f(c * kCK, buf + bi * kCK, min(kCK, S - c * kCK));
+      f(c * CK, buf + bi * CK, min(CK, S - c * CK));
       Grp::sync();  // the whole group is done with buffer bi before it is refilled
       issue(c + NB);
     }
@@ -2012,7 +2013,7 @@ struct KeyStreamG {
 // whose keys are in the L2-resident workspace (too many rows to keep on chip):
 // the select group of the warp-specialised A launch, for long MHA sequences.
 // Same composite-key rule as select_unit / select_onchip; publishes tcs[u].
-template <typename Grp, int NB = 2>
+template <typename Grp, int NB = 2, int CK = kCK>
 __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, uint32_t* kbuf, uint64_t* sbar,
                               unsigned& sphase, uint8_t* scratch, int scratch_bytes, PipeShared& sh, int g = 0) {
   const size_t ug = (size_t)u * p.G + g;  // this (unit, head)'s keys and threshold (per-head GQA: G heads in turn)
@@ -2023,7 +2024,7 @@ __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, ui
   unsigned long long* candA = reinterpret_cast<unsigned long long*>(scratch);
   unsigned long long* candB = candA + cap;
   const uint32_t* keys = p.keys + ug * p.kstride;
-  const KeyStreamG<Grp, NB> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S > 0 ? S : 1, kCK)};
+  const KeyStreamG<Grp, NB, CK> ks{keys, S, p.kstride, kbuf, sbar, &sphase, ceil_div(S > 0 ? S : 1, CK)};
   unsigned long long Tc;
   if (kb <= 0 || kb >= S) {
     Tc = kb <= 0 ? ~0ull : 0ull;
@@ -2192,9 +2193,13 @@ __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned lo
       const int t0 = tid * PER;
       unsigned m = 0;
 #pragma unroll
-      for (int e = 0; e < PER; ++e) {
-        const int j = t0 + e;
-        m |= (j < nrow && comp_key(kc[j], j0 + j) >= Tc ? 1u : 0u) << e;
+      for (int e4 = 0; e4 < PER; e4 += 4) {  // 16-byte loads: a lane's PER keys are contiguous
+        const uint4 kk = *reinterpret_cast<const uint4*>(kc + t0 + e4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = t0 + e4 + e;
+          m |= (j < nrow && comp_key(u4_at(kk, e), j0 + j) >= Tc ? 1u : 0u) << (e4 + e);
+        }
       }
       const unsigned c = __popc(m);
       unsigned tot;
@@ -2221,12 +2226,12 @@ __device__ void emit_lists_global(const PipeParams& p, int u, int S, unsigned lo
 // an entry (head mask << 24 | row), ascending, written in place over the unit's head-0 keys (same rule
 // as emit_lists_global: positions never pass their rows, the chunks in flight lie beyond), plus the half
 // parts' entry offsets and, for diagnostics, each head's own ascending index row.
-template <typename Grp, int G_T, int NB>
+template <typename Grp, int G_T, int NB, int CKE>
 __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint32_t* kbuf, uint64_t* sbar,
                                         unsigned& sphase, PipeShared& sh) {
-  constexpr int C = kCK / G_T;              // rows per chunk (one buffer holds G_T x C keys)
+  constexpr int C = CKE / G_T;              // rows per chunk (one buffer holds G_T x C keys)
   constexpr int PER = C / Grp::kThreads;    // contiguous rows per thread and chunk
-  static_assert(PER >= 1, "chunk too small");
+  static_assert(PER >= 4 && PER % 4 == 0, "a thread's rows are read as whole uint4 groups");
   const int tid = Grp::tid();
   const int G = p.G;
   const int lhs = 31 - __clz(p.Lc / 2);
@@ -2250,7 +2255,7 @@ __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint3
       for (int g = 0; g < G; ++g)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(kbuf + (c % NB) * kCK + g * C)),
+                smem_u32(kbuf + (c % NB) * CKE + g * C)),
             "l"(keys + (size_t)g * p.kstride + base), "r"(bytes), "r"(smem_u32(bar))
             : "memory");
     }
@@ -2265,20 +2270,26 @@ __device__ void emit_lists_global_heads(const PipeParams& p, int u, int S, uint3
       const int bi = c % NB;
       mbar_wait(&sbar[bi], (sphase >> bi) & 1u);
       sphase ^= 1u << bi;
-      const uint32_t* kc = kbuf + bi * kCK;
+      const uint32_t* kc = kbuf + bi * CKE;
       const int j0 = c * C, t0 = tid * PER;
       const int nrow = min(C, S - j0);
       unsigned m[PER];
       unsigned cnt = 0;
 #pragma unroll
-      for (int e = 0; e < PER; ++e) {
-        m[e] = 0u;
-        if (t0 + e < nrow)
+      for (int e = 0; e < PER; ++e) m[e] = 0u;
 #pragma unroll
-          for (int g = 0; g < G_T; ++g)
-            if (g < G && comp_key(kc[g * C + t0 + e], j0 + t0 + e) >= Tc[g]) m[e] |= 1u << g;
-        cnt += m[e] != 0u;
+      for (int g = 0; g < G_T; ++g) {
+        if (g >= G) break;
+#pragma unroll
+        for (int e4 = 0; e4 < PER; e4 += 4) {  // 16-byte loads: a lane's PER keys are contiguous
+          const uint4 kk = *reinterpret_cast<const uint4*>(kc + g * C + t0 + e4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (t0 + e4 + e < nrow && comp_key(u4_at(kk, e), j0 + t0 + e4 + e) >= Tc[g]) m[e4 + e] |= 1u << g;
+        }
       }
+#pragma unroll
+      for (int e = 0; e < PER; ++e) cnt += m[e] != 0u;
       unsigned tot;
       unsigned at = base + block_incl_scan<Grp>(cnt, sh, &tot) - cnt;
       const int r0 = j0 + t0;
@@ -2625,12 +2636,14 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       const uint32_t* keys = kbuf2 + (size_t)b * p.La;
       const long long t0 = (p.trace != nullptr) ? globaltimer() : 0;
       sel_stamp<SelectGrp>(p, u, 0);
-      if constexpr (G_T > 1) {  // per-head GQA: the G heads in turn, thresholds for the B items' key path
+      if constexpr (G_T > 1) {  // per-head GQA: the G heads in turn, then the union emission
+        // (r02: the heads on four 2-warp sub-groups at once measured no faster -- the passes are bound by
+        // the select threads' per-key work, not by L2 latency)
         for (int g = 0; g < p.G; ++g)
           select_global<SelectGrp, kSelNB>(p, u, S, hist2 + ((size_t)b * G_T + g) * HB, kbuf2, sbar, sphase, cand,
                                            p.cand_bytes, sh, g);
         sel_stamp<SelectGrp>(p, u, 4);
-        if (p.lists) emit_lists_global_heads<SelectGrp, G_T, kSelNB>(p, u, S, kbuf2, sbar, sphase, sh);
+        if (p.lists) emit_lists_global_heads<SelectGrp, G_T, 2, kSelNB * kCK / 2>(p, u, S, kbuf2, sbar, sphase, sh);
       } else if constexpr (ONCHIP) {
         select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
         sel_stamp<SelectGrp>(p, u, 4);
