@@ -540,14 +540,26 @@ class DecodeGraph:
     are at replay time (write the next token's inputs into them, then `replay()`).
     Capture runs the step `warmup` + 1 times on a side stream: like any step, each
     run writes the new K_hat / V rows at `rows` (the caller advances rows / lens).
+
+    Host-fed steps: `inputs[layer]` = [(device_tensor, pinned_host_tensor), ...]
+    makes the graph copy that layer's inputs from host memory on a copy stream,
+    each layer waiting only for its own copies, so layer l + 1's transfer overlaps
+    layer l's kernels; `output` = (pinned_host_tensor, device_tensor) copies the
+    result back at the end of the graph.  The host tensors are read / written at
+    replay time.
     """
 
-    def __init__(self, decoders, between=None, warmup: int = 2):
+    def __init__(self, decoders, between=None, warmup: int = 2, inputs=None, output=None):
         if not decoders:
             raise ShapeError("DecodeGraph needs at least one LokiDecoder")
         self.decoders = list(decoders)
         self.between = between
+        if inputs is not None and len(inputs) != len(self.decoders):
+            raise ShapeError(f"{len(inputs)} input lists for {len(self.decoders)} layers")
+        self.inputs = inputs
+        self.output = output
         dev = self.decoders[0].device
+        self._copy = torch.cuda.Stream(dev) if inputs is not None else None
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
@@ -561,10 +573,26 @@ class DecodeGraph:
         torch.cuda.synchronize(dev)
 
     def _run(self):
+        main = torch.cuda.current_stream()
+        events = []
+        if self.inputs is not None:  # every layer's host -> device copies, queued ahead on the copy stream
+            self._copy.wait_stream(main)
+            with torch.cuda.stream(self._copy):
+                for pairs in self.inputs:
+                    for dst, src in pairs:
+                        dst.copy_(src, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self._copy)
+                    events.append(ev)
         for layer, dec in enumerate(self.decoders):
+            if events:
+                main.wait_event(events[layer])
             dec.step()
             if self.between is not None:
                 self.between(layer)
+        if self.output is not None:
+            host, dev_t = self.output
+            host.copy_(dev_t, non_blocking=True)
 
     def replay(self):
         """Launch the captured step on the current stream; returns the last layer's output."""
