@@ -479,7 +479,8 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
     const bool pow2 = ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0;
     const int GS = gqa_ws ? G_T : 1;  // key arrays / histograms per unit in the A launch
     const bool onchip = GS == 1 && ps.La <= env_int("LOKI_ONCHIP_ROWS", 8192) && pow2;
-    // ring stages per stream warp: 3 where they fit (r02: TGT 591 -> 566 us, C2 177 -> 174 us), else 2
+    // ring stages per stream warp: 3 where they fit (r02: 2 -> 3 TGT 591 -> 566 us, C2 177 -> 174 us; 4 measured
+    // no faster at TGT, 567 vs 566 us), else 2
     size_t sw = 0;
     int ow = 0;
     for (int nst = env_int("LOKI_SELECT_STAGES", 3); nst >= 2 && ow < 1; --nst) {

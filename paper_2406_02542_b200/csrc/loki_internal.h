@@ -57,6 +57,9 @@ struct FusedParams {
 // Key-stream buffers of the warp-specialised A launch's select group (16 KB each): the key passes are
 // L2-latency bound, so four chunks are kept in flight (r02: two left a 32K-key pass at ~7 GB/s).
 constexpr int kSelNB = 4;
+// ... in use: four for per-head groups (G passes per unit), two for G = 1 (its shared memory goes to a
+// fourth stream stage instead: r02, TGT)
+__host__ __device__ constexpr int sel_nb(int G_T) { return G_T > 1 ? kSelNB : 2; }
 
 struct PipeParams {
   const float* q_hat;  // [B, Hq, D]

@@ -65,7 +65,7 @@ size_t pipe_select_layout(PipeParams* p, bool onchip, int G_T) {
   p->off_hist = (int)off;
   off = align_up(off + 2 * (size_t)G_T * (1u << p->hbits) * 4, 128);  // [2][G_T][HB]
   p->off_kchip = (int)off;  // on-chip keys [2][La], or the key stream's chunk buffers [kSelNB][kCK]
-  off = align_up(off + (onchip ? 2 * (size_t)p->La : (size_t)kSelNB * kCK) * 4, 128);
+  off = align_up(off + (onchip ? 2 * (size_t)p->La : (size_t)sel_nb(G_T) * kCK) * 4, 128);
   p->off_cand = (int)off;
   p->cand_bytes = (onchip ? 16 : 32) * 1024;  // boundary-bin candidates, two buffers; more -> histogram levels
   off += (size_t)p->cand_bytes;

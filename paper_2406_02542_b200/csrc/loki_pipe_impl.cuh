@@ -2640,19 +2640,20 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
         // (r02: the heads on four 2-warp sub-groups at once measured no faster -- the passes are bound by
         // the select threads' per-key work, not by L2 latency)
         for (int g = 0; g < p.G; ++g)
-          select_global<SelectGrp, kSelNB>(p, u, S, hist2 + ((size_t)b * G_T + g) * HB, kbuf2, sbar, sphase, cand,
+          select_global<SelectGrp, sel_nb(G_T)>(p, u, S, hist2 + ((size_t)b * G_T + g) * HB, kbuf2, sbar, sphase, cand,
                                            p.cand_bytes, sh, g);
         sel_stamp<SelectGrp>(p, u, 4);
-        if (p.lists) emit_lists_global_heads<SelectGrp, G_T, 2, kSelNB * kCK / 2>(p, u, S, kbuf2, sbar, sphase, sh);
+        if (p.lists)
+          emit_lists_global_heads<SelectGrp, G_T, 2, sel_nb(G_T) * kCK / 2>(p, u, S, kbuf2, sbar, sphase, sh);
       } else if constexpr (ONCHIP) {
         select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
         sel_stamp<SelectGrp>(p, u, 4);
         emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
       } else {
-        select_global<SelectGrp, kSelNB>(p, u, S, hist2 + (size_t)b * HB, kbuf2, sbar, sphase, cand, p.cand_bytes,
+        select_global<SelectGrp, sel_nb(G_T)>(p, u, S, hist2 + (size_t)b * HB, kbuf2, sbar, sphase, cand, p.cand_bytes,
                                          sh);
         sel_stamp<SelectGrp>(p, u, 4);
-        if (p.lists) emit_lists_global<SelectGrp, kSelNB>(p, u, S, p.tcs[u], kbuf2, sbar, sphase, sh);
+        if (p.lists) emit_lists_global<SelectGrp, sel_nb(G_T)>(p, u, S, p.tcs[u], kbuf2, sbar, sphase, sh);
       }
       sel_stamp<SelectGrp>(p, u, 5);
       if (tid == 0) {
