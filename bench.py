@@ -745,6 +745,35 @@ def phase_split(wl, decs, reps):
             "timing": "each launch alone, CUDA events, per layer, mean over all layers x reps"}
 
 
+def quality_block(wl, dec):
+    """N3 at config scale (metrics.py:90-133 jaccard_topk, attention.py:145-156 exact_topk_attention): for every
+    (batch, query head) of layer 0, the Jaccard similarity of Loki's selection (leading d PCA columns) and the
+    exact top-k of the full logits (the same ranking kernel with d = D), and the relative error of Loki's
+    output against exact top-k attention and against dense attention."""
+    import torch
+
+    import paper_2406_02542_b200 as L
+    from paper_2406_02542_b200.metrics import _jaccard_rows
+
+    gs = wl.cfg.get("group_select", "per_head")
+    y_l, d_l = L.loki_decode(dec.q_hat, wl.K[0], wl.V[0], wl.lens, d=wl.d, k=wl.k, diagnostics=True,
+                             group_select=gs)
+    y_e, d_e = L.loki_decode(dec.q_hat, wl.K[0], wl.V[0], wl.lens, d=wl.D, k=wl.k, diagnostics=True)
+    y_d = L.dense_decode(dec.q_hat, wl.K[0], wl.V[0], wl.lens)
+    jac = _jaccard_rows(d_l.indices.reshape(-1, wl.k), d_e.indices.reshape(-1, wl.k))
+    rel = lambda a, b: ((a - b).norm(dim=-1) / b.norm(dim=-1)).reshape(-1)  # noqa: E731
+    r_e, r_d = rel(y_l, y_e), rel(y_l, y_d)
+    torch.cuda.synchronize()
+    return {"units": int(jac.numel()), "jaccard_vs_exact_topk_mean": round(float(jac.mean()), 4),
+            "jaccard_vs_exact_topk_min": round(float(jac.min()), 4),
+            "rel_l2_vs_exact_topk_mean": float(f"{float(r_e.mean()):.3e}"),
+            "rel_l2_vs_dense_mean": float(f"{float(r_d.mean()):.3e}"),
+            "what": "layer 0, every (batch, query head): Loki (d = d_f D) vs exact top-k (d = D) selections "
+                    "(Jaccard) and outputs; Loki vs dense attention output.  A property of the synthetic data: "
+                    "rank-16 keys planted before RoPE and cached after it, P calibrated on the pre-RoPE keys, "
+                    "queries N(0, 1) -- diffuse attention the leading PCA columns rank poorly"}
+
+
 def gather_compare(wl, dec, reps):
     """R14 / criterion 7 (reference bench.py:275-321, kernels.py:297-308) at layer scale: sparse exact
     attention over a given selection, fused (the library's gather kernel: rows read in place, scores,
@@ -956,10 +985,11 @@ def main():
     reps = max(10, args.steps // 2)
     attn = attention_block(wl, decs, reps, world, with_dense=not args.no_extras)
     fused_us = attn["loki_attention_us_per_layer"]
-    gcmp = phases = None
+    gcmp = phases = quality = None
     if rank == 0 and world == 1 and not args.no_extras:
         gcmp = gather_compare(wl, decs[0], reps)
         phases = phase_split(wl, decs, 3)
+        quality = quality_block(wl, decs[0])
     append_us = max(0.0, us_layer - fused_us)
     peak, peak_src = peak_gbs()
     traffic = None
@@ -1083,6 +1113,7 @@ def main():
             "parity": parity,
             "gather_compare": gcmp,
             "phases": phases,
+            "quality": quality,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "tgt": tgt,
