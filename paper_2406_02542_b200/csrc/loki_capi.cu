@@ -478,7 +478,9 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
     // (the merge re-derives each head's selection from them), so such calls keep the key path
     const bool pow2 = ((p.Lc / 2) & (p.Lc / 2 - 1)) == 0;
     const int GS = gqa_ws ? G_T : 1;  // key arrays / histograms per unit in the A launch
-    const bool onchip = GS == 1 && ps.La <= env_int("LOKI_ONCHIP_ROWS", 8192) && pow2;
+    // on-chip keys up to 8192 rows; group-shared layers up to 16384 (with two stream stages: C4 shared
+    // 358.6 -> 340.5 us; MHA at 16K loses with two stages, 307.6 -> 368.0 us at B = 16)
+    const bool onchip = GS == 1 && ps.La <= env_int("LOKI_ONCHIP_ROWS", shared ? 16384 : 8192) && pow2;
     // ring stages per stream warp: 3 where they fit (r02: 2 -> 3 TGT 591 -> 566 us, C2 177 -> 174 us; 4 measured
     // no faster at TGT, 567 vs 566 us), else 2
     size_t sw = 0;
