@@ -9,6 +9,7 @@
 
 #include "loki_common.cuh"
 #include "loki_internal.h"
+#include <cstring>
 
 namespace loki {
 long long* g_phase_trace = nullptr;
@@ -578,7 +579,9 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
 }
 
 // phases: bit 0 the A-only launch, bit 1 the B-only launch (split plans; both = the decode step).
-loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream, int phases = 3) {
+// `cached_maps`: the four tensor maps of an earlier call with identical arguments (plan cache).
+loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream, int phases = 3,
+                     const loki::TmaDesc* cached_maps = nullptr, loki::TmaDesc* maps_out = nullptr) {
   const loki_kv_geom& g = a->g;
   if (a->workspace == nullptr || a->workspace_bytes < pl.ws)
     return fail(LOKI_ERR_SHAPE, "workspace of %zu bytes required", pl.ws);
@@ -630,8 +633,14 @@ loki_status run_pipe(const loki_decode_args* a, PipePlan& pl, void* stream, int 
   p.trace = (loki::g_phase_trace != nullptr && p.n_tickets * 4 <= (long long)loki::g_phase_trace_ctas * 8)
                 ? loki::g_phase_trace : nullptr;
   loki::TmaDesc maps[4];
-  if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, p.mma != 0, p.lead_swz, maps))
+  if (cached_maps != nullptr) {
+    for (int i = 0; i < 4; ++i) maps[i] = cached_maps[i];
+  } else if (!loki::encode_pipe_tma(a->K, a->V, g, p.dbox, p.r1, p.split_k ? p.d : 0, p.mma != 0, p.lead_swz,
+                                    maps)) {
     return fail(LOKI_ERR_CUDA, "cuTensorMapEncodeTiled rejected the cache geometry");
+  }
+  if (maps_out != nullptr)
+    for (int i = 0; i < 4; ++i) maps_out[i] = maps[i];
   cudaError_t e = cudaSuccess;
   if (!pl.split && phases != 3) return fail(LOKI_ERR_UNSUPPORTED, "single-launch plan: phases run together");
   if (pl.split) {
@@ -764,14 +773,49 @@ loki_status loki_decode_phase(const loki_decode_args* a, int32_t launches, void*
   return run_pipe(a, pl, stream, launches);
 }
 
-loki_status loki_decode(const loki_decode_args* a, void* stream) {
-  loki_status s = validate(a);
+// Per-thread cache of recent pipe plans and their tensor maps, keyed by the argument block's bytes and
+// the device: a serving loop (LokiDecoder, the HF cache, eager replays) calls with identical arguments every
+// step, so the planning, occupancy queries and four cuTensorMapEncodeTiled calls run once.  Tuning mode
+// (LOKI_TUNING=1: the plan may follow the environment) bypasses it.
+struct PlanCacheEntry {
+  bool valid = false;
+  int dev = -1;
+  loki_decode_args a{};
+  PipePlan pl;
+  loki::TmaDesc maps[4];
+};
+constexpr int kPlanCache = 8;
+thread_local PlanCacheEntry g_plan_cache[kPlanCache];
+thread_local int g_plan_next = 0;
+
+loki_status loki_decode(const loki_decode_args* a_in, void* stream) {
+  loki_status s = validate(a_in);
   if (s != LOKI_OK) return s;
+  const bool cacheable = !tuning_enabled() && loki::g_phase_trace == nullptr;
+  int dev = 0;
+  if (cacheable && cudaGetDevice(&dev) == cudaSuccess) {
+    for (PlanCacheEntry& e : g_plan_cache)
+      if (e.valid && e.dev == dev && std::memcmp(&e.a, a_in, sizeof(loki_decode_args)) == 0)
+        return run_pipe(&e.a, e.pl, stream, 3, e.maps);
+  }
   loki_decode_args a1, a2;
-  a = small_batch_plan(canonical_mode(a, &a1), &a2);
+  const loki_decode_args* a = small_batch_plan(canonical_mode(a_in, &a1), &a2);
   {
     PipePlan pl;
-    if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) return run_pipe(a, pl, stream);
+    if (pipe_eligible(a) && make_pipe_plan(a, &pl) == LOKI_OK) {
+      if (!cacheable || a != a_in) return run_pipe(a, pl, stream);
+      PlanCacheEntry& e = g_plan_cache[g_plan_next];
+      e.valid = false;
+      const loki_status r = run_pipe(a, pl, stream, 3, nullptr, e.maps);
+      if (r == LOKI_OK) {
+        e.a = *a_in;
+        e.dev = dev;
+        e.pl = pl;
+        e.valid = true;
+        g_plan_next = (g_plan_next + 1) % kPlanCache;
+      }
+      return r;
+    }
   }
   if (a->select_mode == LOKI_SELECT_TOPK_SHARED) return shared_unsupported(a);
   loki::Plan plan;
