@@ -29,6 +29,8 @@ CASES = {  # B, Hq, Hkv, S
     "split": (1, 2, 2, 8192),
     "gqa": (1, 8, 2, 8192),
     "shared": (2, 8, 2, 9000),  # group-shared selection (chunked A launch + entry lists)
+    "ws_gqa": (37, 16, 4, 8192),  # 148 units: the warp-specialised per-head A launch (tcgen05 phase 1)
+    "ws_mha": (5, 32, 32, 8192),  # 160 units: the warp-specialised MHA A launch (on-chip keys, lists)
 }
 for name, (B, Hq, Hkv, S) in CASES.items():
     if a.case not in ("all", name):
