@@ -497,6 +497,8 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
       // (units whose keys stay in the workspace publish lists too: the select group streams them back once
       // more and writes the entries in place, so B items copy slices instead of re-deriving them)
       p.lists = (onchip || (pow2 && lists_plan)) ? 1 : 0;
+      // key mode (tuning): on-chip selection publishes only the threshold, B items scan the workspace keys
+      if (onchip && !shared && a->idx_out == nullptr && env_int("LOKI_WS_KEYS", 0) != 0) p.lists = 0;
       pl->ws_groups = GS;
       if (GS > 1 && env_int("LOKI_UMMA", 1) != 0) {  // per-head phase 1 on tcgen05: 128-row tile stages
         const int tile = 128 * p.dbox * 2;

@@ -2523,6 +2523,8 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       S = S < 0 ? 0 : (S > p.S_max ? p.S_max : S);
       uint32_t* hist = hist2 + (size_t)b * G_T * HB;
       uint32_t* keys = ONCHIP ? kbuf2 + (size_t)b * p.La : p.keys + (size_t)u * p.G * p.kstride;
+      // on-chip selection without entry lists: the keys also go to the workspace for the B items
+      uint32_t* kglob = (ONCHIP && !p.lists) ? p.keys + (size_t)u * p.kstride : nullptr;
       for (int j = tid; j < G_T * HB; j += kPT) hist[j] = 0u;
       StreamGrp::sync();
       const int n = S < p.La ? S : p.La;
@@ -2599,7 +2601,8 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
           mbar_wait(&wbar[rp.slot], rp.phase);
           const int box = w + k * kPW;
           const int rows_here = min(R1, n - box * R1);
-          lead_consume_lpr<T, RB>(p, wring + rp.slot * SB, rows_here, q2, keys + box * R1, nullptr,
+          lead_consume_lpr<T, RB>(p, wring + rp.slot * SB, rows_here, q2, keys + box * R1,
+                                  kglob != nullptr ? kglob + box * R1 : nullptr,
                                   approx_u ? approx_u + box * R1 : nullptr, hist, hshift);
           __syncwarp();
           if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
@@ -2648,7 +2651,11 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       } else if constexpr (ONCHIP) {
         select_onchip<1, SelectGrp>(p, u, S, keys, p.La, hist2 + (size_t)b * HB, cand, p.cand_bytes, sh);
         sel_stamp<SelectGrp>(p, u, 4);
-        emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
+        if (p.lists) {
+          emit_lists<1, SelectGrp>(p, u, S, keys, p.La, sh);  // ends with a group barrier
+        } else if (tid == 0) {  // key mode: the B items re-derive their rows from the workspace keys
+          p.tcs[u] = sh.Tc[0];
+        }
       } else {
         select_global<SelectGrp, sel_nb(G_T)>(p, u, S, hist2 + (size_t)b * HB, kbuf2, sbar, sphase, cand, p.cand_bytes,
                                          sh);
