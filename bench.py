@@ -198,6 +198,11 @@ def make_layer(cfg, B, Hkv, dev, gen):
     basis = torch.linalg.qr(torch.randn(Hkv, D, rank_r, device=dev, generator=gen))[0]
     zc = torch.randn(Hkv, S_cal, rank_r, device=dev, generator=gen)
     cal = zc @ basis.transpose(1, 2) + sigma * torch.randn(Hkv, S_cal, D, device=dev, generator=gen)
+    if cfg.get("rotary") == "post":  # post-rotary PCA: calibrate on the keys RoPE'd at their positions
+        ac = torch.arange(S_cal, device=dev, dtype=torch.float64)[:, None] * inv[None, :]
+        cc, sc = torch.cos(ac).float(), torch.sin(ac).float()
+        lo_c, hi_c = cal[..., :half], cal[..., half:]
+        cal = torch.cat([lo_c * cc - hi_c * sc, lo_c * sc + hi_c * cc], dim=-1)
     cal = cal.double()
     cal = cal - cal.mean(dim=1, keepdim=True)
     cov = cal.transpose(1, 2) @ cal / (S_cal - 1)
@@ -654,7 +659,7 @@ def config_block(cfg, args, world, d, k):
     return {"workload": f"{cfg['name']}: {cfg['desc']}", "layers": cfg["layers"], "global_batch": cfg["B"],
             "seq_len": cfg["S"], "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"], "head_dim": cfg["D"],
             "k_f": cfg["k_f"], "d_f": cfg["d_f"], "d": d, "k": k, "cache_dtype": cfg.get("cache_dtype", "bf16"),
-            "rotary": f"pre-rotary PCA, rotate-then-project, base {cfg['base']:g}",
+            "rotary": f"{cfg.get('rotary', 'pre')}-rotary PCA, rotate-then-project, base {cfg['base']:g}",
             "l2": "inputs larger than L2 (KV per layer >> 126 MB); no flush",
             "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
             **({"gqa_queries": cfg.get("gqa_queries", "independent"),
@@ -948,13 +953,15 @@ def main():
     ap.add_argument("--cache-dtype", default="bf16", choices=["bf16", "f32"],
                     help="KV cache storage (f32: the exact-reference configuration, SIMT consumers)")
     ap.add_argument("--layers", type=int, default=0, help="override the config's layer count")
+    ap.add_argument("--rotary", default="pre", choices=["pre", "post"],
+                    help="PCA calibrated on pre- or post-RoPE keys (the cache always holds RoPE(k) . P)")
     ap.add_argument("--group-select", default="per_head", choices=["per_head", "shared"],
                     help="GQA selection: per query head (the reference's semantics) or one per KV group "
                          "on the summed group query (opt-in mode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config], gqa_queries=args.gqa_queries, group_select=args.group_select,
-               name=args.config, cache_dtype=args.cache_dtype)
+               name=args.config, cache_dtype=args.cache_dtype, rotary=args.rotary)
     if args.layers > 0:
         cfg["layers"] = args.layers
     if args.impl == "reference":
