@@ -467,7 +467,9 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
   const bool gqa_ws = G_T > 1 && !shared && g.dtype == LOKI_DTYPE_BF16 && (p.lead_swz == 64 || p.lead_swz == 128) &&
                       env_int("LOKI_SELECT_WS_GQA", 1) != 0;
   if (pl->split && !dense && ((G_T == 1 || shared) ? g1_lead : gqa_ws) && !p.spec && !p.split_k &&
-      env_int("LOKI_SELECT_WS", 1) != 0 && units >= sm_count()) {
+      env_int("LOKI_SELECT_WS", 1) != 0 && units >= env_int("LOKI_WS_MIN_UNITS", G_T > 1 ? 96 : sm_count())) {
+    // (query groups from 96 units: C5s' 128 units, shared 898 -> 837 us, per-head 2683 -> 2511 us, even with
+    // 20 SMs idle in the A launch -- the chunked launch's serial per-unit selection costs more)
     // The warp-specialised A launch (one 16-warp CTA per SM, one whole unit per item): a stream group
     // streams unit i's lead columns while a select group selects unit i - 1, so the selection never
     // idles the loads.  Units of <= 8192 rows keep their keys on chip and publish ordered entry lists
