@@ -212,8 +212,14 @@ def make_layer(cfg, B, Hkv, dev, gen):
     vecs = vecs * torch.sign(torch.gather(vecs, 1, pick))
     P = vecs.float().contiguous()  # [Hkv, D, D], columns = principal directions
     cdt = torch.float32 if cfg.get("cache_dtype") == "f32" else torch.bfloat16
-    K = torch.empty(B, Hkv, S, D, device=dev, dtype=cdt)
-    V = torch.randn(B, Hkv, S, D, device=dev, generator=gen).to(cdt)
+    if cfg.get("kv_layout") == "interleaved":  # [B, Hkv, S, 2, D]: a row's K and V adjacent in HBM
+        KV = torch.empty(B, Hkv, S, 2, D, device=dev, dtype=cdt)
+        K, V = KV[:, :, :, 0], KV[:, :, :, 1]
+        for h in range(Hkv):
+            V[:, h] = torch.randn(B, S, D, device=dev, generator=gen).to(cdt)
+    else:
+        K = torch.empty(B, Hkv, S, D, device=dev, dtype=cdt)
+        V = torch.randn(B, Hkv, S, D, device=dev, generator=gen).to(cdt)
     for h in range(Hkv):
         z = torch.randn(B, S, rank_r, device=dev, generator=gen)
         kp = z @ basis[h].T + sigma * torch.randn(B, S, D, device=dev, generator=gen)
@@ -658,7 +664,7 @@ def union_rows(wl, dec):
 def config_block(cfg, args, world, d, k):
     return {"workload": f"{cfg['name']}: {cfg['desc']}", "layers": cfg["layers"], "global_batch": cfg["B"],
             "seq_len": cfg["S"], "q_heads": cfg["Hq"], "kv_heads": cfg["Hkv"], "head_dim": cfg["D"],
-            "k_f": cfg["k_f"], "d_f": cfg["d_f"], "d": d, "k": k, "cache_dtype": cfg.get("cache_dtype", "bf16"),
+            "k_f": cfg["k_f"], "d_f": cfg["d_f"], "d": d, "k": k, "cache_dtype": cfg.get("cache_dtype", "bf16"), "kv_layout": cfg.get("kv_layout", "separate"),
             "rotary": f"{cfg.get('rotary', 'pre')}-rotary PCA, rotate-then-project, base {cfg['base']:g}",
             "l2": "inputs larger than L2 (KV per layer >> 126 MB); no flush",
             "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
@@ -953,6 +959,9 @@ def main():
     ap.add_argument("--cache-dtype", default="bf16", choices=["bf16", "f32"],
                     help="KV cache storage (f32: the exact-reference configuration, SIMT consumers)")
     ap.add_argument("--layers", type=int, default=0, help="override the config's layer count")
+    ap.add_argument("--kv-layout", default="separate", choices=["separate", "interleaved"],
+                    help="KV cache layout: separate K and V caches, or one [B, Hkv, S, 2, D] cache whose "
+                         "K and V rows are adjacent (512 B row gathers)")
     ap.add_argument("--rotary", default="pre", choices=["pre", "post"],
                     help="PCA calibrated on pre- or post-RoPE keys (the cache always holds RoPE(k) . P)")
     ap.add_argument("--group-select", default="per_head", choices=["per_head", "shared"],
@@ -961,7 +970,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config], gqa_queries=args.gqa_queries, group_select=args.group_select,
-               name=args.config, cache_dtype=args.cache_dtype, rotary=args.rotary)
+               name=args.config, cache_dtype=args.cache_dtype, rotary=args.rotary, kv_layout=args.kv_layout)
     if args.layers > 0:
         cfg["layers"] = args.layers
     if args.impl == "reference":

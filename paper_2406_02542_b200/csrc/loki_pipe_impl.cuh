@@ -1423,6 +1423,9 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
     int row = -1;  // -1: out of bounds, zero-filled
     const int t = st * R + lane;
     if (lane < R && t < n) row = row_base + (int)(ents[t] & 0xFFFFFFu);
+    // warp-uniform operands (tma_gather4_u): no per-instruction waterfall loop around the TMA issues
+    const uint32_t ds = __shfl_sync(0xffffffffu, smem_u32(dst), 0);
+    const uint32_t bs = __shfl_sync(0xffffffffu, smem_u32(&wbar[at.slot]), 0);
 #pragma unroll
     for (int qq = 0; qq < R / 4; ++qq) {
       const int a0 = __shfl_sync(0xffffffffu, row, 4 * qq);
@@ -1432,12 +1435,12 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
       if (lane == 0) {
 #pragma unroll
         for (int h = 0; h < NH; ++h)
-          tma_gather4(dst + h * HW + qq * 512, vrow_map, 64 * h, a0, a1, a2, a3, &wbar[at.slot]);
+          tma_gather4_u(ds + h * HW + qq * 512, vrow_map, 64 * h, a0, a1, a2, a3, bs);
 #pragma unroll
         for (int j = 0; j < ka; ++j)
-          tma_gather4(dst + (NH + j) * HW + qq * 512, krow_map, kc0 + 64 * j, a0, a1, a2, a3, &wbar[at.slot]);
+          tma_gather4_u(ds + (NH + j) * HW + qq * 512, krow_map, kc0 + 64 * j, a0, a1, a2, a3, bs);
         if constexpr (kbp > 0)
-          tma_gather4(dst + (NH + ka) * HW + qq * 256, krow64_map, D_T - 32, a0, a1, a2, a3, &wbar[at.slot]);
+          tma_gather4_u(ds + (NH + ka) * HW + qq * 256, krow64_map, D_T - 32, a0, a1, a2, a3, bs);
       }
     }
   };

@@ -59,6 +59,17 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
 }
+// Shared-memory operands as 32-bit addresses.  TMA instructions take uniform registers: operands that ptxas
+// cannot prove warp-uniform cost a per-instruction waterfall loop (ELECT, R2UR.BROADCAST, BRA.U.ANY), so
+// callers broadcast them from lane 0 first (__shfl_sync(~0u, x, 0) results are known uniform).
+__device__ __forceinline__ void tma_gather4_u(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+                                              int r3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }

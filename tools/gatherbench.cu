@@ -5,6 +5,8 @@
 //   mode 1: same rows as two 128 B halves, SWIZZLE_128B (the tensor-core layout)
 //   mode 2: 4-D-style lead boxes: 64 B of every 256 B row (L2 promotion 64 B)
 //   mode 3: contiguous 256 B rows (dense)
+//   mode 4: gather4 of 512 B rows (K and V rows interleaved: one selected row = K row + V row)
+//   mode 5: the interleaved rows of mode 4 fetched as the kernel's B items do: four 128 B swizzled halves
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/gb tools/gatherbench.cu -lcuda
 //   /tmp/gb <mode> <warps> <stages> <stage_kb> <ctas_per_sm>
 #include <cuda.h>
@@ -58,7 +60,7 @@ struct Args {
 };
 
 __global__ void bench(Args a, const __grid_constant__ CUtensorMap full, const __grid_constant__ CUtensorMap half,
-                      const __grid_constant__ CUtensorMap lead) {
+                      const __grid_constant__ CUtensorMap lead, const __grid_constant__ CUtensorMap wide, const __grid_constant__ CUtensorMap whalf) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su(smem_raw) & 1023u)) & 1023u);
   __shared__ int s_item;
@@ -72,14 +74,14 @@ __global__ void bench(Args a, const __grid_constant__ CUtensorMap full, const __
   unsigned phase = 0;
   int used = 0;
   // rows per stage: mode 0 sb/256, mode 1 sb/256 (two halves), mode 2 sb/64 lead rows, mode 3 sb/256
-  const int rps = (a.mode == 2) ? a.sb / 64 : a.sb / 256;
+  const int rps = (a.mode == 2) ? a.sb / 64 : (a.mode >= 4 ? a.sb / 512 : a.sb / 256);
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(a.ticket, 1);
     __syncthreads();
     const int it = s_item;
     __syncthreads();
     if (it >= a.items) break;
-    const int nrows = (a.mode == 0 || a.mode == 1) ? a.sel_per_item : a.rows_per_item;
+    const int nrows = (a.mode != 2 && a.mode != 3) ? a.sel_per_item : a.rows_per_item;
     const int nstage = (nrows + rps - 1) / rps;
     const int* idx = a.idx + (size_t)it * a.sel_per_item;
     const int base = it * a.rows_per_item;
@@ -99,7 +101,11 @@ __global__ void bench(Args a, const __grid_constant__ CUtensorMap full, const __
         const int r0 = __shfl_sync(~0u, row, 4 * q), r1 = __shfl_sync(~0u, row, 4 * q + 1);
         const int r2 = __shfl_sync(~0u, row, 4 * q + 2), r3 = __shfl_sync(~0u, row, 4 * q + 3);
         if (lane == 0) {
-          if (a.mode == 0) {
+          if (a.mode == 4) {
+            g4(dst + q * 2048, &wide, 0, r0, r1, r2, r3, &bars[sl]);
+          } else if (a.mode == 5) {
+            for (int hh = 0; hh < 4; ++hh) g4(dst + hh * rps * 128 + q * 512, &whalf, 64 * hh, r0, r1, r2, r3, &bars[sl]);
+          } else if (a.mode == 0) {
             g4(dst + q * 1024, &full, 0, r0, r1, r2, r3, &bars[sl]);
           } else {
             g4(dst + q * 512, &half, 0, r0, r1, r2, r3, &bars[sl]);
@@ -145,8 +151,9 @@ int main(int argc, char** argv) {
   const int items = (int)(total_rows / rows_per_item);
   const int sel = rows_per_item / 4;
   uint8_t* buf;
-  CK(cudaMalloc(&buf, total_rows * 256));
-  CK(cudaMemset(buf, 1, total_rows * 256));
+  const size_t row_bytes = mode >= 4 ? 512 : 256;
+  CK(cudaMalloc(&buf, total_rows * row_bytes));
+  CK(cudaMemset(buf, 1, total_rows * row_bytes));
   std::vector<int> h((size_t)items * sel);
   std::mt19937 rng(1);
   std::vector<int> perm(rows_per_item);
@@ -166,7 +173,10 @@ int main(int argc, char** argv) {
   cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
   EncFn enc = (EncFn)fn;
-  CUtensorMap full, half, lead;
+  CUtensorMap full, half, lead, wide, whalf;
+  cuuint64_t wdims[2] = {256, total_rows};
+  cuuint64_t wstr[1] = {512};
+  cuuint32_t bwide[2] = {256, 1};
   cuuint64_t dims[2] = {128, total_rows};
   cuuint64_t str[1] = {256};
   cuuint32_t es[2] = {1, 1};
@@ -178,7 +188,11 @@ int main(int argc, char** argv) {
       enc(&half, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, bhalf, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ||
       enc(&lead, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, blead, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)) {
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ||
+      enc(&wide, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, wdims, wstr, bwide, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ||
+      enc(&whalf, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, wdims, wstr, bhalf, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)) {
     printf("encode failed\n");
     return 1;
   }
@@ -197,7 +211,7 @@ int main(int argc, char** argv) {
   for (int rep = 0; rep < 4; ++rep) {
     CK(cudaMemset(ticket, 0, 4));
     cudaEventRecord(e0);
-    bench<<<sms * cps, nw * 32, smem>>>(a, full, half, lead);
+    bench<<<sms * cps, nw * 32, smem>>>(a, full, half, lead, wide, whalf);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -205,7 +219,7 @@ int main(int argc, char** argv) {
     best = std::min(best, ms);
   }
   CK(cudaGetLastError());
-  double bytes = (mode == 0 || mode == 1) ? (double)items * sel * 256 : (mode == 2 ? (double)total_rows * 64 : (double)total_rows * 256);
+  double bytes = mode >= 4 ? (double)items * sel * 512 : (mode == 0 || mode == 1) ? (double)items * sel * 256 : (mode == 2 ? (double)total_rows * 64 : (double)total_rows * 256);
   printf("mode %d warps %d stages %d stage_kb %d ctas/sm %d (occ %d): %.1f us, %.0f GB/s\n", mode, nw, nst, sb / 1024, cps,
          occ, best * 1e3, bytes / (best * 1e-3) / 1e9);
   return 0;
