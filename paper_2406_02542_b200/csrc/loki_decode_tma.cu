@@ -139,11 +139,11 @@ __global__ void __launch_bounds__(NW * 32) fused_decode_tma_kernel(
     const int nbox = ceil_div(c.n_local, R1);
     const unsigned box_bytes = (unsigned)(R1 * p.dbox * E);
     const int mine = nbox > w ? ceil_div(nbox - w, NW) : 0;  // boxes w, w + NW, ...
-    auto issue = [&](int k, const RingPos& at) {
-      mbar_expect_tx(&wbar[at.slot], box_bytes);
-      tma_box4d(wring + at.slot * SB, &lead_map, 0, c.s0 + (w + k * NW) * R1, c.hk, c.b, &wbar[at.slot]);
+    auto issue = [&](int k, const RingPos& at) {  // every lane (tma_box4d_warp: warp-uniform operands)
+      tma_box4d_warp(wring + at.slot * SB, &lead_map, 0, c.s0 + (w + k * NW) * R1, c.hk, c.b, &wbar[at.slot],
+                     box_bytes);
     };
-    if (lane == 0) {
+    {
       RingPos q = rp;
       for (int k = 0; k < nsw && k < mine; ++k, q.advance(1)) issue(k, q);
     }
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(NW * 32) fused_decode_tma_kernel(
         default: consume_lead<T, G_T, VEC, 32>(p, c, tile, i * R1, rows_here, q1, lane); break;
       }
       __syncwarp();  // every lane is done with the slot before it is refilled
-      if (lane == 0 && k + nsw < mine) issue(k + nsw, rp);
+      if (k + nsw < mine) issue(k + nsw, rp);
     }
   }
   __syncthreads();
@@ -201,6 +201,9 @@ __global__ void __launch_bounds__(NW * 32) fused_decode_tma_kernel(
     const int st = w + k * NW;
     uint8_t* dst = wring + at.slot * SB;
     if (lane == 0) mbar_expect_tx(&wbar[at.slot], stage_bytes);
+    // warp-uniform TMA operands (tma_gather4_u): no per-instruction waterfall loop
+    const uint32_t ds = __shfl_sync(0xffffffffu, smem_u32(dst), 0);
+    const uint32_t bs = __shfl_sync(0xffffffffu, smem_u32(&wbar[at.slot]), 0);
     if (!gather) {
       if (lane == 0) {
         tma_box4d(dst, &kbox_map, 0, c.s0 + st * R3, c.hk, c.b, &wbar[at.slot]);
@@ -216,8 +219,8 @@ __global__ void __launch_bounds__(NW * 32) fused_decode_tma_kernel(
         const int r2 = __shfl_sync(0xffffffffu, row, 4 * qq + 2);
         const int r3 = __shfl_sync(0xffffffffu, row, 4 * qq + 3);
         if (lane == 0) {
-          tma_gather4(dst + qq * 4 * ROWB, &krow_map, 0, r0, r1, r2, r3, &wbar[at.slot]);
-          tma_gather4(dst + R3 * ROWB + qq * 4 * ROWB, &vrow_map, 0, r0, r1, r2, r3, &wbar[at.slot]);
+          tma_gather4_u(ds + qq * 4 * ROWB, &krow_map, 0, r0, r1, r2, r3, bs);
+          tma_gather4_u(ds + R3 * ROWB + qq * 4 * ROWB, &vrow_map, 0, r0, r1, r2, r3, bs);
         }
       }
     }

@@ -70,6 +70,28 @@ __device__ __forceinline__ void tma_gather4_u(uint32_t dst, const CUtensorMap* m
       "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_box4d_u(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+          "r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+// Called by every lane of a warp: the operands are broadcast from lane 0 (warp-uniform for ptxas) and lane 0
+// arms the barrier and issues the box
+__device__ __forceinline__ void tma_box4d_warp(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                               uint64_t* bar, unsigned bytes) {
+  const uint32_t ds = __shfl_sync(0xffffffffu, smem_u32(dst), 0);
+  const uint32_t bs = __shfl_sync(0xffffffffu, smem_u32(bar), 0);
+  c1 = __shfl_sync(0xffffffffu, c1, 0);
+  c2 = __shfl_sync(0xffffffffu, c2, 0);
+  c3 = __shfl_sync(0xffffffffu, c3, 0);
+  if ((threadIdx.x & 31) == 0) {
+    mbar_expect_tx(bar, bytes);
+    tma_box4d_u(ds, map, c0, c1, c2, c3, bs);
+  }
+}
 __device__ __forceinline__ void prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
