@@ -187,3 +187,53 @@ def test_decode_graph_with_host_inputs_matches_manual_copies():
         dec.step()
     torch.cuda.synchronize()
     assert torch.equal(got, decs[-1].out.cpu())
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,S,gs", [(2, 8, 8, 9000, "per_head"),    # split MHA layer (entry lists)
+                                           (4, 4, 4, 4096, "per_head"),    # one launch
+                                           (1, 32, 32, 4096, "per_head"),  # cluster-per-unit plan
+                                           (2, 16, 4, 9000, "per_head"),   # per-head GQA (tcgen05 phase 1)
+                                           (2, 16, 4, 9000, "shared")])    # group-shared selection
+def test_interleaved_kv_layout_matches_separate(B, Hq, Hkv, S, gs):
+    """bench --kv-layout interleaved: K and V as views of one [B, Hkv, S, 2, D] buffer (a row's K and V
+    adjacent in HBM; row stride 2 D) run in place through the C-ABI's strides and give the same bits as
+    separate packed caches -- selections, approx scores and outputs."""
+    D = 128
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    KV = torch.randn(B, Hkv, S, 2, D, device="cuda", generator=gen).to(torch.bfloat16)
+    K, V = KV[:, :, :, 0], KV[:, :, :, 1]
+    assert K.stride(2) == 2 * D
+    q = torch.randn(B, Hq, D, device="cuda", generator=gen)
+    y, diag = L.loki_decode(q, K, V, None, d=32, k_f=0.25, diagnostics=True, group_select=gs)
+    y0 = L.loki_decode(q, K, V, None, d=32, k_f=0.25, group_select=gs)
+    y2, diag2 = L.loki_decode(q, K.contiguous(), V.contiguous(), None, d=32, k_f=0.25, diagnostics=True,
+                              group_select=gs)
+    torch.cuda.synchronize()
+    assert torch.equal(diag.indices, diag2.indices)
+    assert torch.equal(diag.approx_scores, diag2.approx_scores)
+    assert torch.equal(y, y2) and torch.equal(y0, y)
+
+
+def test_interleaved_kv_layout_decoder_step():
+    """K0 appends into the interleaved views (the new token's K and V rows land side by side) and the
+    decode step that follows equals the one on separate caches bit for bit."""
+    B, Hq, Hkv, D, S = 2, 8, 8, 128, 9000
+    gen = torch.Generator(device="cuda").manual_seed(22)
+    KV = torch.randn(B, Hkv, S, 2, D, device="cuda", generator=gen).to(torch.bfloat16)
+    Ks, Vs = KV[:, :, :, 0].contiguous(), KV[:, :, :, 1].contiguous()
+    P = torch.linalg.qr(torch.randn(Hkv, D, D, device="cuda", generator=gen))[0].contiguous()
+    rows = torch.full((B,), S - 1, dtype=torch.int32, device="cuda")
+    lens = torch.full((B,), S, dtype=torch.int32, device="cuda")
+    q = torch.randn(B, Hq, D, device="cuda", generator=gen)
+    k = torch.randn(B, Hkv, D, device="cuda", generator=gen)
+    v = torch.randn(B, Hkv, D, device="cuda", generator=gen)
+    pos = torch.full((B,), S - 1, dtype=torch.int64, device="cuda")
+    outs = []
+    for K, V in ((KV[:, :, :, 0], KV[:, :, :, 1]), (Ks, Vs)):
+        dec = L.LokiDecoder(K, V, P, Hq=Hq, d=32, k_f=0.25, rows=rows, lens=lens, q_raw=q.clone(), k_raw=k.clone(),
+                            v_new=v.clone(), rope_mode=1, positions=pos)
+        dec.step()
+        torch.cuda.synchronize()
+        outs.append((dec.out.clone(), K[:, :, S - 1].clone(), V[:, :, S - 1].clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
