@@ -1389,6 +1389,10 @@ __device__ void stream_B_simt(const PipeParams& p, const CUtensorMap* krow_map, 
 // keys) is added to the logit and the leading d columns are not fetched again.
 // Per stage, with the 8 rows as M rows 0..7 of m16n8k16 (rows 8..15 zero):
 //   S^T[8 x 8] = K[8 x D'] . Qc[D' x 8]  and  O^T[D x 8] += V^T[D x 8] . P^T[8 x 8]
+// MHA (G = 1, kc0 = 0) folds the head dimension's upper half into the idle rows instead (kFold): M rows
+// 8..15 of q.K are the same 8 rows' dims [D/2, D) against query columns 2..3 (hi / lo of q[D/2:]), and the
+// k rows 8..15 of P.V are the stage rows again against the upper dims, P in columns 2..3 -- every mma
+// does useful work, half as many mmas per row (r03).
 // (fp32 accumulate).  Columns carry (head, hi / lo part): q * qscale and the
 // softmax weights are split into two bf16 terms, so both products keep ~2^-17
 // relative accuracy.  G <= 4: column 2h + part;  G == 8: columns = heads, hi
@@ -1449,11 +1453,14 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
     for (int k = 0; k < nsw && k < mine; ++k, qp.advance(1)) issue(k, qp);
   }
   // B operand of S^T = K . Qc: lane holds Qc[16 ks + 2 t4 + {0, 1, 8, 9}][g8]
+  // (kFold: column g8 = 2 half + part holds q[half * D / 2 + 16 ks + ...], half in {0, 1}; KF k-steps)
+  constexpr bool kFold = G_T == 1 && KC0 == 0;
+  constexpr int KF = kFold ? KS / 2 : KS;  // k-steps of q.K == m-tiles of P.V
   uint32_t qb[KS][2], ql[G_T == 8 ? KS : 1][2];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
-    const int k0 = kc0 + 16 * ks + 2 * t4;
-    const int head = kSplitCols ? (g8 >> 1) : g8;
+    const int k0 = kFold ? (g8 >> 1) * (D_T / 2) + 16 * ks + 2 * t4 : kc0 + 16 * ks + 2 * t4;
+    const int head = kFold ? (g8 < 4 && ks < KF ? 0 : G) : (kSplitCols ? (g8 >> 1) : g8);
     float v[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -1491,9 +1498,21 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
     const int st = w + k * kPW;
     const uint32_t sb = smem_u32(wring + rp.slot * SB);
     float S[4] = {0.f, 0.f, 0.f, 0.f}, S2[4] = {0.f, 0.f, 0.f, 0.f};
+    if constexpr (kFold) {  // x4: rows 0..7 x {dims [16 ks, +16), dims [D/2 + 16 ks, +16)}
+      const int hiX = (lane >> 3) & 1, khX = lane >> 4;
+#pragma unroll
+      for (int ks = 0; ks < KF; ++ks) {
+        const int dim0 = hiX * (D_T / 2) + 16 * ks + 8 * khX;
+        uint32_t a[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                     : "r"(swz128(sb + (NH + (dim0 >> 6)) * HW, rX, (dim0 & 63) >> 3)));
+        mma_bf16((ks & 1) ? S2 : S, a, qb[ks][0], qb[ks][1]);
+      }
+    }
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      if constexpr (true) {
+      if constexpr (!kFold) {
         if (ks >= KSK) continue;
         uint32_t addr;
         if (ks < 4 * ka) {  // 128 B piece ks / 4
@@ -1520,8 +1539,15 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
     float x[NHL], pr[NHL], sc[NHL];
 #pragma unroll
     for (int j = 0; j < NHL; ++j) {
-      const int head = kSplitCols ? t4 : 2 * t4 + j;
-      x[j] = kSplitCols ? (S[0] + S2[0]) + (S[1] + S2[1]) : S[j] + S2[j];
+      // (kFold: lane t4 = 0 holds row g8's lower-half sum, t4 = 1 the upper half (M row g8 + 8, columns
+      // 2..3); both lanes then carry the row's score and the same softmax state)
+      const int head = kFold ? (t4 < 2 ? 0 : G) : (kSplitCols ? t4 : 2 * t4 + j);
+      if constexpr (kFold) {
+        x[j] = t4 == 0 ? (S[0] + S2[0]) + (S[1] + S2[1]) : (S[2] + S2[2]) + (S[3] + S2[3]);
+        x[j] += __shfl_xor_sync(0xffffffffu, x[j], 1);
+      } else {
+        x[j] = kSplitCols ? (S[0] + S2[0]) + (S[1] + S2[1]) : S[j] + S2[j];
+      }
       const bool ok = head < G && ((eA >> (24 + head)) & 1u);
       if (split && ok) x[j] += apx[head * p.Lc + tA];  // phase-1 partial over the first d columns
       float tm = ok ? x[j] : -CUDART_INF_F;
@@ -1533,14 +1559,14 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
       pr[j] = ok ? exp2f(x[j] - mn) : 0.f;
       l[j] = l[j] * sc[j] + pr[j];
       m[j] = mn;
-      if (want_logits && ok) p.logits[((size_t)u * G + head) * p.S_cap + (eA & 0xFFFFFFu)] = x[j];
+      if (want_logits && ok && (!kFold || t4 == 0)) p.logits[((size_t)u * G + head) * p.S_cap + (eA & 0xFFFFFFu)] = x[j];
     }
     bool same = true;
 #pragma unroll
     for (int j = 0; j < NHL; ++j) same &= sc[j] == 1.f;
     if (!__all_sync(0xffffffffu, same)) {
 #pragma unroll
-      for (int mt = 0; mt < KS; ++mt) {
+      for (int mt = 0; mt < KF; ++mt) {
         O[mt][0] *= sc[0];
         O[mt][2] *= sc[0];
         O[mt][1] *= sc[NHL - 1];
@@ -1549,9 +1575,28 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
     }
     // B operand P^T: lane holds P[rows 2 t4, 2 t4 + 1][column g8] (rows 8..15 do not exist);
     // (row r, lane head slot) lives in lane r * 4 + head slot
-    const int src0 = (2 * t4) * 4 + (g8 >> 1), src1 = src0 + 4;
+    const int src0 = (2 * t4) * 4 + (kFold ? 0 : (g8 >> 1)), src1 = src0 + 4;
     uint32_t pb, pl = 0u;
-    if (kSplitCols) {
+    if constexpr (kFold) {  // k rows 0..7: P in columns 0..1; k rows 8..15 (same rows, upper dims): columns 2..3
+      const float v0 = __shfl_sync(0xffffffffu, pr[0], src0);
+      const float v1 = __shfl_sync(0xffffffffu, pr[0], src1);
+      const bool lo = g8 & 1;
+      const uint32_t pk = pack_bf16(lo ? bf16_lo(v0) : v0, lo ? bf16_lo(v1) : v1);
+      pb = g8 < 2 ? pk : 0u;
+      pl = (g8 == 2 || g8 == 3) ? pk : 0u;
+#pragma unroll
+      for (int mt = 0; mt < KF; ++mt) {  // x4.trans: V^T dims [16 mt, +16) and [D/2 + 16 mt, +16) of rows 0..7
+        const int dim = 16 * mt + (cX << 3) + (lane >> 4) * (D_T / 2);
+        uint32_t a[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+                     : "r"(swz128(sb + (dim >> 6) * HW, rX, (dim & 63) >> 3)));
+        mma_bf16(O[mt], a, pb, pl);
+      }
+      __syncwarp();
+      if (k + nsw < mine) issue(k + nsw, rp);
+      continue;
+    } else if (kSplitCols) {
       const float v0 = __shfl_sync(0xffffffffu, pr[0], src0);
       const float v1 = __shfl_sync(0xffffffffu, pr[0], src1);
       const bool lo = g8 & 1;
@@ -1588,7 +1633,18 @@ __device__ void stream_B_mma(const PipeParams& p, const CUtensorMap* krow_map, c
 #pragma unroll
   for (int j = 0; j < NHL; ++j) {
     const int head = kSplitCols ? t4 : 2 * t4 + j;
-    if (head < G) {
+    if (kFold && t4 < 2) {  // lane t4 holds output dims t4 * D / 2 + [0, D / 2)
+      float* dstp = wpart + (size_t)w * (D_T + 2) + t4 * (D_T / 2);
+#pragma unroll
+      for (int mt = 0; mt < KF; ++mt) {
+        dstp[16 * mt + g8] = O[mt][0] + O[mt][1];
+        dstp[16 * mt + g8 + 8] = O[mt][2] + O[mt][3];
+      }
+      if (g8 == 0 && t4 == 0) {
+        dstp[D_T] = m[j];
+        dstp[D_T + 1] = l[j];
+      }
+    } else if (!kFold && head < G) {
       float* dstp = wpart + ((size_t)w * G_T + head) * (D_T + 2);
 #pragma unroll
       for (int mt = 0; mt < KS; ++mt) {
