@@ -2815,9 +2815,11 @@ __global__ void __launch_bounds__(2 * kPT, 1) pipe_select_kernel(const PipeParam
       }
       sel_stamp<SelectGrp>(p, u, 5);
       if (tid == 0) {
-        __threadfence();  // the group's list stores (ordered by the barrier) before the release
-        st_release(&p.ctrl[2 + 4 * (size_t)u + 2], 1u);
+        // the buffer is free as soon as the group's barrier has passed: hand it back first (the stream group
+        // waits on it when the selection is the longer side, C2); then the release store, cumulative over the
+        // group's list stores ordered by that barrier (no separate fence: st.release.gpu is one)
         mbar_arrive(&empty[b]);
+        st_release(&p.ctrl[2 + 4 * (size_t)u + 2], 1u);
         if (p.trace != nullptr) {  // one row per unit: {select start, end, smid | kind 3, select start}
           unsigned smid;
           asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
