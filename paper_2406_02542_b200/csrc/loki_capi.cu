@@ -516,6 +516,12 @@ loki_status make_pipe_plan(const loki_decode_args* a_in, PipePlan* pl) {
       pl->sel_layout = ps;
       pl->smem1 = sw;
       pl->grid1 = sm_count() * ow;
+      // MHA: leave some SMs to the B launch from the layer's start -- B CTAs there drain the first selected
+      // units while the A launch streams (r02 sweep, LOKI_SELECT_GRID after the faster on-chip selection: C2
+      // 148 -> 138 A CTAs, attention 165.9 -> 162.7 us; TGT 148 -> 120, 550.4 -> 545.9 us; group-shared GQA
+      // does not gain: C4 shared 343 -> 359 us at 136)
+      if (G_T == 1 && !shared && ow == 1 && units >= 2 * sm_count())
+        pl->grid1 = sm_count() - (a->S_max >= 32768 ? sm_count() * 3 / 16 : sm_count() / 16 + 1);
       const int g1 = env_int("LOKI_SELECT_GRID", 0);  // tuning: fewer A CTAs leave SMs to the B launch
       if (g1 > 0 && g1 < pl->grid1) pl->grid1 = g1;
     }
