@@ -2195,23 +2195,37 @@ __device__ void select_global(const PipeParams& p, int u, int S, uint32_t* h, ui
         if (tid == 0) sh.ncand = 0;
         Grp::sync();
         ks.run([&](int j0, const uint32_t* kc, int nrow) {
-          for (int i0 = 0; i0 < nrow; i0 += 4 * Grp::kThreads) {
-            const int il = i0 + 4 * tid;
-            uint4 kk = make_uint4(0u, 0u, 0u, 0u);
-            if (il < nrow) kk = *reinterpret_cast<const uint4*>(kc + il);
-            unsigned hit = 0;
+          // (r02: the chunk's U uint4 groups per thread first, then one warp scan and one shared atomic per warp
+          // and chunk -- as select_onchip; a scan + atomic chain per 128 rows made this pass ~18 us at 32K rows)
+          constexpr int U = CK / (4 * Grp::kThreads) > 0 ? CK / (4 * Grp::kThreads) : 1;
+          for (int i0 = 0; i0 < nrow; i0 += 4 * U * Grp::kThreads) {
+            uint4 kk[U];
+            unsigned hit[U];
+            int c = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              hit |= (il + e < nrow && (comp_key(u4_at(kk, e), j0 + il + e) >> sh64) == P ? 1u : 0u) << e;
-            if (__any_sync(0xffffffffu, hit != 0u)) {
+            for (int v = 0; v < U; ++v) {
+              const int il = i0 + 4 * (tid + v * Grp::kThreads);
+              kk[v] = make_uint4(0u, 0u, 0u, 0u);
+              if (il < nrow) kk[v] = *reinterpret_cast<const uint4*>(kc + il);
+              hit[v] = 0u;
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                hit[v] |= (il + e < nrow && (comp_key(u4_at(kk[v], e), j0 + il + e) >> sh64) == P ? 1u : 0u) << e;
+              c += __popc(hit[v]);
+            }
+            if (__any_sync(0xffffffffu, c != 0)) {
               int tot;
-              const int ex = warp_excl_scan(__popc(hit), &tot);
+              const int ex = warp_excl_scan(c, &tot);
               int at = 0;
               if (lane == 0) at = atomicAdd(&sh.ncand, tot);
               at = __shfl_sync(0xffffffffu, at, 0) + ex;
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if ((hit >> e) & 1u) candA[at++] = comp_key(u4_at(kk, e), j0 + il + e);
+              for (int v = 0; v < U; ++v) {
+                const int il = i0 + 4 * (tid + v * Grp::kThreads);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if ((hit[v] >> e) & 1u) candA[at++] = comp_key(u4_at(kk[v], e), j0 + il + e);
+              }
             }
           }
         });
